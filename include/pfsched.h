@@ -1,0 +1,194 @@
+/*
+ * pfsched.h — C-ABI of libpfsched.so: the data-parallel hot path of the
+ * Past-Future scheduler (Gong et al., arXiv 2507.10150), batched over many
+ * independent scheduler instances, on NVIDIA B200 (sm_100a).
+ *
+ * Citations are PAPER.md line numbers of /root/reference/PAPER.md (LaTeX source)
+ * with the LaTeX labels (Eq.(eq:5), Alg.(alg:sche), Eq.(eq:1)-(eq:3)); readings
+ * of silent/ambiguous passages are numbered C-1..C-19 in DESIGN.md §3.
+ *
+ * The three calls of the paper's problem statement (Alg.1 inputs/outputs,
+ * PAPER.md:212-213):
+ *   pf_update_history  "records the actual output lengths of historical requests
+ *                      ... L_h = {l_h^0..l_h^w} where w is the window size"
+ *                      (Eq.(eq:5) PAPER.md:197-201)
+ *   pf_estimate_peak   future required memory M* of the running batch,
+ *                      Eq.(eq:1)-(eq:3), with each running
+ *                      request's l̂ re-sampled from P(l > l_t) (Alg.1 lines 3-6,
+ *                      PAPER.md:216-220)
+ *   pf_admit           Alg.1 in full: predictions for running
+ *                      and queued requests, then the longest FIFO queue prefix
+ *                      whose M* fits the capacity M, early return at the first
+ *                      failure
+ *
+ * Exact integer semantics (no floating point anywhere):
+ *   history     w output lengths per window, FIFO; every value in [1, Lmax] (C-1, C-2)
+ *   prediction  for a request with l_t generated tokens (l_t = 0 for queued, C-16):
+ *               gt = sorted{h ∈ L_h : h > l_t} (C-4 strict); if gt is empty
+ *               l̂ = max_new (C-5) else l̂ = gt[⌊u·|gt| / 2^32⌋] (C-3);
+ *               l̂ = min(l̂, max_new) (C-6). With R repetitions the prediction
+ *               is the max of the R samples (C-9).
+ *   u           PF_MODE_QUANTILE: u = quantile_u for every request.
+ *               PF_MODE_SAMPLE:   K = mix64(seed ^ tick·0xD1B54A32D192ED03 ^ inst·0x9E3779B97F4A7C15)
+ *               u_rep = lowbias32(lo32(K) ^ hi32(K) ^ lo32((slot·R + rep)·0x9E3779B9)),
+ *               u = max_rep u_rep; slot = s for the s-th running request (0-based),
+ *               k + j − 1 for the j-th queued request (1-based); inst = global id (C-8).
+ *   peak        a = l_p + l_t, r = l̂ − l_t; occupancy at tick τ ≥ 0 is
+ *               O(τ) = Σ_{r_e ≥ τ} (a_e + τ) ("after growth, before removal",
+ *               PAPER.md:262, C-10); M* = max_τ O(τ) = max_i (Σ_{j≤i} a_j + r_i·i)
+ *               over the r-descending order (Eq.(eq:1)-(eq:3)); empty set → 0.
+ *   admission   p* = the largest p ∈ [0, q] such that for every p' ≤ p
+ *               10^4·M*(R ∪ Q[1..p']) ≤ (10^4 − reserved_bp)·M (C-12 '≤' PAPER.md:226,
+ *               C-13 reserved ratio PAPER.md:342, C-14 early return PAPER.md:231).
+ *               M* is monotone in p, so this is also the largest single p that fits.
+ *
+ * Conventions for every call:
+ *   - Array arguments are caller-owned DEVICE pointers (e.g. torch tensor
+ *     data_ptr()), int32 unless stated, densely packed. Inputs are read-only,
+ *     outputs are fully overwritten; nothing is retained after the call.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream). All work is
+ *     enqueued on it; no call synchronises the host except pf_create, pf_destroy,
+ *     pf_get_device_error and pf_export_history.
+ *   - A context is not thread-safe; calls on one context must be stream-ordered.
+ *   - Host-checkable problems return a negative pf_status synchronously and
+ *     enqueue nothing; pf_last_error() then describes it (thread-local).
+ *   - Data-dependent violations found on the device do not stop the call: the
+ *     offending instance's outputs (or history row's update) are skipped/set to −1
+ *     and a sticky device error word records the first (code, instance/row)
+ *     (first writer wins) — read it with pf_get_device_error (PF_DERR_* codes).
+ */
+#ifndef PFSCHED_H
+#define PFSCHED_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_ABI_VERSION 1
+
+typedef struct pf_ctx pf_ctx;
+
+typedef enum {
+  PF_OK = 0,
+  PF_EINVAL = -1,  /* NULL required pointer, bad size or parameter            */
+  PF_ERANGE = -2,  /* declared bounds exceed what the kernels support/overflow */
+  PF_ESTATE = -3,  /* call not valid in this context mode / sequence           */
+  PF_ECUDA = -4,   /* a CUDA runtime call failed (message in pf_last_error)    */
+  PF_ENOMEM = -6   /* device allocation failed                                 */
+} pf_status;
+
+enum { PF_MODE_SAMPLE = 0, PF_MODE_QUANTILE = 1 };
+
+/* Device error codes (sticky word, see pf_get_device_error). */
+enum {
+  PF_DERR_NONE = 0,
+  PF_DERR_COMPLETION = 1,  /* completion length ∉ [1, Lmax]: that row is not updated    */
+  PF_DERR_OFFSETS = 2,     /* CSR offsets decreasing or k+q > max_entries               */
+  PF_DERR_MAX_NEW = 3,     /* max_new ∉ [1, Lmax]                                       */
+  PF_DERR_INPUT_LEN = 4,   /* l_p ∉ [0, max_input_len]                                  */
+  PF_DERR_GENERATED = 5,   /* l_t ∉ [0, max_new − 1]                                    */
+  PF_DERR_CAPACITY = 6     /* capacity < 0                                              */
+};
+
+typedef struct {
+  int32_t n_instances;     /* local instances on this device (>= 1)                            */
+  int32_t window;          /* per-instance mode: w >= 1 per instance (C-1, default 1000,
+                              PAPER.md:192/:295). Shared mode: the group's global window W,
+                              W % 8 == 0, split into 8 shard rings of W/8 (C-18).               */
+  int32_t max_len;         /* Lmax: output lengths live in [1, Lmax]; 1 <= Lmax <= 32767     */
+  int32_t max_input_len;   /* declared bound on l_p (>= 0)                                    */
+  int32_t max_entries;     /* declared bound on k+q per instance, 1..4096                     */
+  int32_t n_groups;        /* 0 = per-instance histories; G > 0 = shared-group histories      */
+  const int32_t* group_off;/* shared mode: device [G+1]; local instances of group g are
+                              [group_off[g], group_off[g+1]) (group-major layout). Copied.     */
+  int64_t instance_base;   /* per-instance mode: global id of local instance 0 (hash key)     */
+  int32_t members_per_group; /* shared mode: global id of local instance l in group g is      */
+  int32_t member_base;       /*   g·members_per_group + member_base + (l − group_off[g])      */
+  int32_t mode;            /* PF_MODE_SAMPLE | PF_MODE_QUANTILE                               */
+  uint32_t quantile_u;     /* u in quantile mode (0x80000000 = median rank)                   */
+  int32_t repetitions;     /* R >= 1 (C-9)                                                     */
+  int32_t reserved_bp;     /* reserved ratio in basis points, 0..9999 (C-13)                   */
+  uint64_t seed;           /* sampling-mode seed (C-8)                                         */
+  int32_t rank, nranks;    /* shared mode: this rank owns shards {s in 0..7 : s % nranks == rank} */
+} pf_config;
+
+/* Create a context and its device history state.
+ * init_history: device, oldest first, nullable (NULL ⇒ every slot = Lmax, C-2,
+ *   "initialize the output length distribution using the preset maximum output
+ *   length"). Layout: per-instance mode [n_instances × window];
+ *   shared mode [G × shards_owned × W/8] in pf_update_history row order.
+ *   Values must lie in [1, Lmax] (checked; PF_EINVAL otherwise).
+ * Host-checked: n, w, Lmax, max_entries, R, reserved_bp, mode, rank/nranks
+ *   ranges, nranks divides 8, and the int32 overflow bound
+ *   max_entries·(max_input_len + 2·Lmax) < 2^31. Synchronises `stream`. */
+pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* stream,
+                    pf_ctx** out);
+
+/* Free all device state owned by the context (synchronises the device). */
+pf_status pf_destroy(pf_ctx* ctx);
+
+/* Record completed output lengths: for each history row, append
+ * comp_len[comp_off[row] .. comp_off[row+1]) in order, evicting the oldest entry
+ * whenever the row holds more than its window (FIFO, C-1). With more completions
+ * than the window only the last `window` survive.
+ * rows = n_instances (per-instance mode) or G·shards_owned (shared mode, rows
+ * ordered group-major, owned shard minor). comp_off: device [rows+1], comp_len:
+ * device [total]. A row containing a length ∉ [1, Lmax] is left unchanged and
+ * PF_DERR_COMPLETION is recorded.
+ * Shared mode: after the local update the owned-shard group histograms are
+ * written to the exchange buffer; with nranks == 1 the group tables are rebuilt
+ * here; with nranks > 1 the caller must sum-all-reduce the exchange buffer across
+ * ranks (e.g. NCCL on `stream`) and then call pf_commit_history. */
+pf_status pf_update_history(pf_ctx* ctx, const int32_t* comp_off, const int32_t* comp_len,
+                            int32_t total, void* stream);
+
+/* Shared mode only: the int32 [G × (Lmax+1)] device buffer that must be
+ * all-reduced (sum) across ranks between pf_update_history and pf_commit_history.
+ * Owned by the context. PF_ESTATE in per-instance mode. */
+pf_status pf_exchange_buffer(pf_ctx* ctx, int32_t** buf, int64_t* count);
+
+/* Shared mode only: rebuild the group CDF / sorted-window tables from the
+ * (all-reduced) exchange buffer. No-op in per-instance mode. */
+pf_status pf_commit_history(pf_ctx* ctx, void* stream);
+
+/* M*(R) per instance (Eq.(eq:1)-(eq:3)) after re-predicting every running
+ * request (Alg.1 lines 3-6). run_off: [n+1]; input_len, generated: [run_off[n]];
+ * max_new: [n]; peak_out: [n]; pred_out: nullable [run_off[n]] = l̂ per running
+ * request in input order. Equals pf_admit's peak_running_out for the same tick. */
+pf_status pf_estimate_peak(pf_ctx* ctx, const int32_t* run_off, const int32_t* input_len,
+                           const int32_t* generated, const int32_t* max_new, uint32_t tick,
+                           int32_t* peak_out, int32_t* pred_out, void* stream);
+
+/* Algorithm 1 per instance. q_off: [n+1], q_input_len: [q_off[n]] (FIFO order),
+ * capacity: [n] (M, tokens). Outputs: admitted_out [n] = p*; peak_out [n] =
+ * M*(R ∪ Q[1..p*]) (= M*(R) when p* = 0, which may exceed the capacity when the
+ * running batch is already over-committed); peak_running_out nullable [n] = M*(R);
+ * pred_run_out nullable [run_off[n]]; pred_q_out nullable [q_off[n]] (every queued
+ * request, admitted or not). */
+pf_status pf_admit(pf_ctx* ctx, const int32_t* run_off, const int32_t* input_len,
+                   const int32_t* generated, const int32_t* q_off, const int32_t* q_input_len,
+                   const int32_t* max_new, const int32_t* capacity, uint32_t tick,
+                   int32_t* admitted_out, int32_t* peak_out, int32_t* peak_running_out,
+                   int32_t* pred_run_out, int32_t* pred_q_out, void* stream);
+
+/* Read (and keep) the sticky device error word; synchronises `stream`. */
+pf_status pf_get_device_error(pf_ctx* ctx, int32_t* code, int32_t* index, void* stream);
+
+/* Reset the sticky device error word (enqueued on `stream`). */
+pf_status pf_clear_device_error(pf_ctx* ctx, void* stream);
+
+/* Copy the history rings, oldest first, to device rows_out [rows × row_window]
+ * (checkpoint / test hook; same layout as init_history). Enqueued on `stream`. */
+pf_status pf_export_history(pf_ctx* ctx, int32_t* rows_out, void* stream);
+
+/* Describes the last failing call on this thread ("" if none). */
+const char* pf_last_error(void);
+
+int32_t pf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFSCHED_H */

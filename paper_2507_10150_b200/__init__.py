@@ -1,0 +1,12 @@
+"""paper_2507_10150_b200 — B200-native (sm_100a) batched hot path of the Past-Future
+scheduler (arXiv 2507.10150): history window update, future-peak KV-cache estimation
+and FIFO admission over many independent scheduler instances.
+
+The computation lives in libpfsched.so (CUDA kernels behind the C-ABI declared in
+include/pfsched.h); ``binding`` is a ctypes marshalling layer with the same names.
+"""
+from .binding import (PF_MODE_QUANTILE, PF_MODE_SAMPLE, PFError, Scheduler, load, LIB_PATH,
+                      SYMBOLS)
+
+__all__ = ["Scheduler", "PFError", "load", "LIB_PATH", "SYMBOLS", "PF_MODE_SAMPLE",
+           "PF_MODE_QUANTILE"]

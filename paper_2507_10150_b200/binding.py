@@ -1,0 +1,185 @@
+"""Thin ctypes binding of libpfsched.so (include/pfsched.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels
+behind the C-ABI. Tensors are passed as device pointers (``data_ptr()``) with
+torch's current CUDA stream. There is no CPU fallback: if the library or a GPU
+is missing, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpfsched.so")
+
+PF_MODE_SAMPLE, PF_MODE_QUANTILE = 0, 1
+DERR = {0: "none", 1: "completion", 2: "offsets", 3: "max_new", 4: "input_len", 5: "generated",
+        6: "capacity"}
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+
+
+class PFConfig(ctypes.Structure):
+    _fields_ = [
+        ("n_instances", _i32), ("window", _i32), ("max_len", _i32), ("max_input_len", _i32),
+        ("max_entries", _i32), ("n_groups", _i32), ("group_off", _vp), ("instance_base", ctypes.c_int64),
+        ("members_per_group", _i32), ("member_base", _i32), ("mode", _i32),
+        ("quantile_u", ctypes.c_uint32), ("repetitions", _i32), ("reserved_bp", _i32),
+        ("seed", ctypes.c_uint64), ("rank", _i32), ("nranks", _i32),
+    ]
+
+
+_lib = None
+SYMBOLS = ("pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer", "pf_commit_history",
+           "pf_estimate_peak", "pf_admit", "pf_get_device_error", "pf_clear_device_error",
+           "pf_export_history", "pf_last_error", "pf_abi_version")
+
+
+def load(path: str = LIB_PATH):
+    """Load libpfsched.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} not found: run __graft_entry__.build() (no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    L.pf_abi_version.restype = _i32
+    L.pf_last_error.restype = ctypes.c_char_p
+    L.pf_create.argtypes = [P(PFConfig), _vp, _vp, P(_vp)]
+    L.pf_destroy.argtypes = [_vp]
+    L.pf_update_history.argtypes = [_vp, _vp, _vp, _i32, _vp]
+    L.pf_exchange_buffer.argtypes = [_vp, P(_vp), P(ctypes.c_int64)]
+    L.pf_commit_history.argtypes = [_vp, _vp]
+    L.pf_estimate_peak.argtypes = [_vp, _vp, _vp, _vp, _vp, ctypes.c_uint32, _vp, _vp, _vp]
+    L.pf_admit.argtypes = [_vp] + [_vp] * 7 + [ctypes.c_uint32] + [_vp] * 6
+    L.pf_get_device_error.argtypes = [_vp, P(_i32), P(_i32), _vp]
+    L.pf_clear_device_error.argtypes = [_vp, _vp]
+    L.pf_export_history.argtypes = [_vp, _vp, _vp]
+    for s in SYMBOLS:
+        if s not in ("pf_abi_version", "pf_last_error"):
+            getattr(L, s).restype = _i32
+    assert L.pf_abi_version() == 1
+    _lib = L
+    return L
+
+
+class PFError(RuntimeError):
+    pass
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        raise PFError(f"{what} failed with status {st}: {load().pf_last_error().decode()}")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda or t.dtype != torch.int32 or not t.is_contiguous():
+        raise PFError("expected a contiguous int32 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Scheduler:
+    """One pf_ctx: device history state for n instances (or G shared groups)."""
+
+    def __init__(self, *, n_instances: int, window: int, max_len: int, max_input_len: int,
+                 max_entries: int, n_groups: int = 0, group_off: Optional[torch.Tensor] = None,
+                 instance_base: int = 0, members_per_group: int = 0, member_base: int = 0,
+                 mode: int = PF_MODE_SAMPLE, quantile_u: int = 0x80000000, repetitions: int = 1,
+                 reserved_bp: int = 0, seed: int = 0, rank: int = 0, nranks: int = 1,
+                 init_history: Optional[torch.Tensor] = None):
+        L = load()
+        self.cfg = PFConfig(n_instances, window, max_len, max_input_len, max_entries, n_groups,
+                            None if group_off is None else group_off.data_ptr(), instance_base,
+                            members_per_group, member_base, mode, quantile_u & 0xFFFFFFFF,
+                            repetitions, reserved_bp, seed & 0xFFFFFFFFFFFFFFFF, rank, nranks)
+        self._keep = (group_off, init_history)
+        h = ctypes.c_void_p()
+        _check(L.pf_create(ctypes.byref(self.cfg), _ptr(init_history), _stream(), ctypes.byref(h)),
+               "pf_create")
+        self._h = h
+        self.n = n_instances
+        self.shared = n_groups > 0
+        self.rows = n_groups * (8 // nranks) if self.shared else n_instances
+        self.row_window = window // 8 if self.shared else window
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            load().pf_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the three calls
+    def update_history(self, comp_off: torch.Tensor, comp_len: torch.Tensor):
+        _check(load().pf_update_history(self._h, _ptr(comp_off), _ptr(comp_len) if comp_len.numel() else None,
+                                        int(comp_len.numel()), _stream()), "pf_update_history")
+
+    def exchange_buffer(self) -> torch.Tensor:
+        """Shared mode: the int32 [G, Lmax+1] device buffer to all-reduce (sum)."""
+        buf, cnt = ctypes.c_void_p(), ctypes.c_int64()
+        _check(load().pf_exchange_buffer(self._h, ctypes.byref(buf), ctypes.byref(cnt)), "pf_exchange_buffer")
+        return _wrap_device_int32(buf.value, cnt.value)
+
+    def commit_history(self):
+        _check(load().pf_commit_history(self._h, _stream()), "pf_commit_history")
+
+    def estimate_peak(self, run_off, input_len, generated, max_new, tick: int, *, peak_out=None,
+                      pred_out=None):
+        if peak_out is None:
+            peak_out = torch.empty(self.n, dtype=torch.int32, device=run_off.device)
+        _check(load().pf_estimate_peak(self._h, _ptr(run_off), _ptr(input_len), _ptr(generated),
+                                       _ptr(max_new), tick & 0xFFFFFFFF, _ptr(peak_out), _ptr(pred_out),
+                                       _stream()), "pf_estimate_peak")
+        return peak_out
+
+    def admit(self, run_off, input_len, generated, q_off, q_input_len, max_new, capacity, tick: int, *,
+              admitted_out=None, peak_out=None, peak_running_out=None, pred_run_out=None,
+              pred_q_out=None):
+        dev = run_off.device
+        if admitted_out is None:
+            admitted_out = torch.empty(self.n, dtype=torch.int32, device=dev)
+        if peak_out is None:
+            peak_out = torch.empty(self.n, dtype=torch.int32, device=dev)
+        _check(load().pf_admit(self._h, _ptr(run_off), _ptr(input_len), _ptr(generated), _ptr(q_off),
+                               _ptr(q_input_len), _ptr(max_new), _ptr(capacity), tick & 0xFFFFFFFF,
+                               _ptr(admitted_out), _ptr(peak_out), _ptr(peak_running_out),
+                               _ptr(pred_run_out), _ptr(pred_q_out), _stream()), "pf_admit")
+        return admitted_out, peak_out
+
+    def device_error(self):
+        code, idx = _i32(), _i32()
+        _check(load().pf_get_device_error(self._h, ctypes.byref(code), ctypes.byref(idx), _stream()),
+               "pf_get_device_error")
+        return code.value, idx.value
+
+    def clear_device_error(self):
+        _check(load().pf_clear_device_error(self._h, _stream()), "pf_clear_device_error")
+
+    def export_history(self) -> torch.Tensor:
+        out = torch.empty((self.rows, self.row_window), dtype=torch.int32, device="cuda")
+        _check(load().pf_export_history(self._h, _ptr(out), _stream()), "pf_export_history")
+        return out
+
+
+def _wrap_device_int32(ptr: int, count: int) -> torch.Tensor:
+    """Zero-copy int32 CUDA tensor view of a context-owned device buffer."""
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (count,), "typestr": "<i4", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_CAI(), device="cuda")

@@ -1,0 +1,234 @@
+// pf_history.cuh — history-window kernels of libpfsched (sm_100a).
+// "During serving, it records the actual output lengths of historical requests ...
+//  L_h = {l_h^0 ... l_h^w} where w is the window size", and the
+// counter function C(l, L_h) of Eq.(eq:5).
+//
+// Device representations:
+//   ring  [rows × row_window]  FIFO contents, head = index of the oldest entry
+//   per-instance, w ≤ Lmax+1: sorted [n × w] ascending copy of the ring (the
+//                              inverse CDF is then S[base + ρ])
+//   per-instance, w > Lmax+1: hist [n × (Lmax+1)] counts C(l, L_h)
+//   shared groups:            phist [G × (Lmax+1)] counts over owned shards;
+//                              after the all-reduce, C_g (cumulative counts) and
+//                              S_g (sorted group window) tables.
+#pragma once
+#include "pf_common.cuh"
+
+namespace pf {
+
+// ---------------------------------------------------------------- init
+__global__ void init_ring_kernel(int32_t* ring, int64_t total, const int32_t* init, int max_len,
+                                 int* n_bad) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int v = init ? init[x] : max_len;
+    if (v < 1 || v > max_len) {
+      atomicAdd(n_bad, 1);
+      v = max_len;
+    }
+    ring[x] = v;
+  }
+}
+
+// Bitonic sort of each row (create time only): CTA per row, P2 = pow2 ≥ w in smem.
+__global__ void sort_rows_kernel(const int32_t* ring, int32_t* sorted, int w, int P2) {
+  extern __shared__ int32_t buf[];
+  const int64_t row = blockIdx.x;
+  for (int x = threadIdx.x; x < P2; x += blockDim.x)
+    buf[x] = x < w ? ring[row * w + x] : 0x7FFFFFFF;
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int x = threadIdx.x; x < P2; x += blockDim.x) {
+        const int y = x ^ stride;
+        if (y > x) {
+          const bool up = (x & size) == 0;
+          const int a = buf[x], b = buf[y];
+          if ((a > b) == up) {
+            buf[x] = b;
+            buf[y] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int x = threadIdx.x; x < w; x += blockDim.x) sorted[row * w + x] = buf[x];
+}
+
+// Histogram rows: hist[row*(Lmax+1) + v] += 1 for each ring value (rows_per_hist
+// consecutive ring rows feed one histogram row).
+__global__ void hist_rows_kernel(const int32_t* ring, int64_t total, int row_window,
+                                 int rows_per_hist, int max_len, int32_t* hist) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = x / row_window;
+    atomicAdd(&hist[(row / rows_per_hist) * (max_len + 1) + ring[x]], 1);
+  }
+}
+
+// ---------------------------------------------------------------- update
+// Validate one row's completions (warp-cooperative). Returns false if any ∉ [1, Lmax].
+__device__ __forceinline__ bool row_valid(const int32_t* comp_len, int c0, int c1, int max_len,
+                                          int lane) {
+  bool bad = c1 < c0;
+  for (int t = c0 + lane; !bad && t < c1; t += 32) {
+    const int v = comp_len[t];
+    bad = bad || v < 1 || v > max_len;
+  }
+  return !__any_sync(0xffffffffu, bad);
+}
+
+// #{x < v} and #{x ≤ v} over ascending global row S[0..w).
+__device__ __forceinline__ int lower_bound_g(const int32_t* S, int w, int v) {
+  int lo = 0, len = w;
+  while (len > 0) {
+    int half = len >> 1;
+    bool right = S[lo + half] < v;
+    lo = right ? lo + half + 1 : lo;
+    len = right ? len - half - 1 : half;
+  }
+  return lo;
+}
+__device__ __forceinline__ int upper_bound_g(const int32_t* S, int w, int v) {
+  int lo = 0, len = w;
+  while (len > 0) {
+    int half = len >> 1;
+    bool right = S[lo + half] <= v;
+    lo = right ? lo + half + 1 : lo;
+    len = right ? len - half - 1 : half;
+  }
+  return lo;
+}
+
+// Per-instance rings with a maintained sorted copy (w ≤ Lmax+1). Warp per row;
+// completions applied one at a time in order: evict v_old = ring[head], append
+// v_new, and move the sorted copy's elements between the two positions by one.
+__global__ void update_sorted_kernel(int n_rows, int w, int max_len, const int32_t* comp_off,
+                                     const int32_t* comp_len, int32_t* ring, int32_t* head,
+                                     int32_t* sorted, int* err) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n_rows) return;
+  const int c0 = comp_off[row], c1 = comp_off[row + 1];
+  if (c1 == c0) return;
+  if (!row_valid(comp_len, c0, c1, max_len, lane)) {
+    if (lane == 0) raise_error(err, PF_BAD_COMPLETION, row);
+    return;
+  }
+  int32_t* R = ring + (int64_t)row * w;
+  int32_t* S = sorted + (int64_t)row * w;
+  int h = head[row];
+  for (int t = c0; t < c1; ++t) {
+    const int v_new = comp_len[t];
+    const int v_old = R[h];
+    __syncwarp();
+    if (lane == 0) R[h] = v_new;
+    h = (h + 1 == w) ? 0 : h + 1;
+    if (v_new == v_old) continue;
+    if (v_new > v_old) {
+      // remove first v_old at i, insert v_new at j: S[i..j-1] <- S[i+1..j], S[j] = v_new
+      const int i = lower_bound_g(S, w, v_old);
+      const int j = upper_bound_g(S, w, v_new) - 1;
+      for (int x0 = i; x0 < j; x0 += 32) {
+        const int x = x0 + lane;
+        const int v = (x < j) ? S[x + 1] : 0;
+        __syncwarp();
+        if (x < j) S[x] = v;
+        __syncwarp();
+      }
+      if (lane == 0) S[j] = v_new;
+    } else {
+      // remove last v_old at i, insert v_new at j: S[j+1..i] <- S[j..i-1], S[j] = v_new
+      const int i = upper_bound_g(S, w, v_old) - 1;
+      const int j = upper_bound_g(S, w, v_new);
+      for (int x1 = i; x1 > j; x1 -= 32) {
+        const int x = x1 - lane;
+        const int v = (x > j) ? S[x - 1] : 0;
+        __syncwarp();
+        if (x > j) S[x] = v;
+        __syncwarp();
+      }
+      if (lane == 0) S[j] = v_new;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) head[row] = h;
+}
+
+// Rings feeding histograms: per-instance (w > Lmax+1, rows_per_hist = 1, plain
+// stores) or shared groups (rows_per_hist = shards owned, atomics since several
+// shard rows of one group update its histogram concurrently). Warp per row.
+__global__ void update_hist_kernel(int n_rows, int row_window, int rows_per_hist, int max_len,
+                                   const int32_t* comp_off, const int32_t* comp_len,
+                                   int32_t* ring, int32_t* head, int32_t* hist, int* err) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n_rows) return;
+  const int c0 = comp_off[row], c1 = comp_off[row + 1];
+  if (c1 == c0) return;
+  if (!row_valid(comp_len, c0, c1, max_len, lane)) {
+    if (lane == 0) raise_error(err, PF_BAD_COMPLETION, row);
+    return;
+  }
+  if (lane != 0) return;
+  int32_t* R = ring + (int64_t)row * row_window;
+  int32_t* H = hist + (int64_t)(row / rows_per_hist) * (max_len + 1);
+  int h = head[row];
+  for (int t = c0; t < c1; ++t) {
+    const int v_new = comp_len[t];
+    const int v_old = R[h];
+    R[h] = v_new;
+    h = (h + 1 == row_window) ? 0 : h + 1;
+    if (rows_per_hist == 1) {
+      H[v_old] -= 1;
+      H[v_new] += 1;
+    } else {
+      atomicSub(&H[v_old], 1);
+      atomicAdd(&H[v_new], 1);
+    }
+  }
+  head[row] = h;
+}
+
+// Group tables from the (all-reduced) group histogram H_g: C_g[l] = Σ_{l'≤l} H_g[l']
+// and the sorted window S_g (S_g[x] = l for x ∈ [C_g[l−1], C_g[l])). CTA per group.
+template <int T>
+__global__ void __launch_bounds__(T) group_tables_kernel(const int32_t* H, int max_len, int W,
+                                                         int32_t* gC, int32_t* gS) {
+  __shared__ int scratch[64];
+  const int g = blockIdx.x;
+  const int nb = max_len + 1;
+  const int32_t* h = H + (int64_t)g * nb;
+  int32_t* C = gC + (int64_t)g * nb;
+  int32_t* S = gS + (int64_t)g * W;
+  const int per = (nb + T - 1) / T;
+  const int lo = threadIdx.x * per, hi = min(nb, lo + per);
+  int s = 0;
+  for (int l = lo; l < hi; ++l) s += h[l];
+  int v[1] = {s}, tot[1];
+  block_exclusive_add<T, 1>(v, tot, scratch);
+  int acc = v[0];
+  for (int l = lo; l < hi; ++l) {
+    const int prev = acc;
+    acc += h[l];
+    C[l] = acc;
+    for (int x = prev; x < acc && x < W; ++x) S[x] = l;
+  }
+}
+
+// Export rings oldest-first.
+__global__ void export_rows_kernel(const int32_t* ring, const int32_t* head, int n_rows,
+                                   int row_window, int32_t* out) {
+  const int64_t total = (int64_t)n_rows * row_window;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = x / row_window;
+    const int t = (int)(x - row * row_window);
+    int src = head[row] + t;
+    if (src >= row_window) src -= row_window;
+    out[x] = ring[row * row_window + src];
+  }
+}
+
+}  // namespace pf

@@ -1,0 +1,389 @@
+// pfsched.cu — the C-ABI of libpfsched.so (include/pfsched.h): context, argument
+// validation, and launches of the sm_100a kernels in pf_history.cuh / pf_admit.cuh.
+// No torch types cross this boundary; every array is a caller-owned device pointer.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/pfsched.h"
+#include "pf_admit.cuh"
+#include "pf_history.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pf_status fail(pf_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define PF_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(e_ == cudaErrorMemoryAllocation ? PF_ENOMEM : PF_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                  \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+enum Layout { LAYOUT_SORTED = 0, LAYOUT_HIST = 1, LAYOUT_GROUP = 2 };
+
+// Admit-kernel variants: (threads per instance, items per thread).
+typedef void (*AdmitFn)(pf::AdmitParams);
+struct Variant {
+  int T, IPT;
+  AdmitFn fn[3];
+};
+
+#define PF_VARIANT(T, IPT)                                                                   \
+  {T, IPT, {pf::admit_kernel<T, IPT, pf::LOOK_SORTED>, pf::admit_kernel<T, IPT, pf::LOOK_HIST>, \
+            pf::admit_kernel<T, IPT, pf::LOOK_GROUP>}}
+const Variant kVariants[] = {
+    PF_VARIANT(128, 1), PF_VARIANT(128, 2), PF_VARIANT(128, 4), PF_VARIANT(256, 3),
+    PF_VARIANT(256, 4), PF_VARIANT(256, 5), PF_VARIANT(256, 8), PF_VARIANT(256, 16),
+};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
+}  // namespace
+
+struct pf_ctx {
+  pf_config cfg;
+  int layout;
+  int n_rows, row_window, rows_per_hist, shards_owned;
+  int32_t* ring = nullptr;
+  int32_t* head = nullptr;
+  int32_t* sorted = nullptr;  // LAYOUT_SORTED
+  int32_t* hist = nullptr;    // LAYOUT_HIST: per instance; LAYOUT_GROUP: partial (owned shards)
+  int32_t* xbuf = nullptr;    // LAYOUT_GROUP exchange buffer [G × (Lmax+1)]
+  int32_t* gC = nullptr;
+  int32_t* gS = nullptr;
+  int32_t* dist_of = nullptr;
+  int32_t* group_off = nullptr;
+  int* err = nullptr;  // [2] code, index
+  int* scratch = nullptr;
+  int variant;
+  size_t admit_smem;
+  int n_bins, bin_shift;
+};
+
+namespace {
+
+void free_ctx(pf_ctx* c) {
+  if (!c) return;
+  for (void* p : {(void*)c->ring, (void*)c->head, (void*)c->sorted, (void*)c->hist,
+                  (void*)c->xbuf, (void*)c->gC, (void*)c->gS, (void*)c->dist_of,
+                  (void*)c->group_off, (void*)c->err, (void*)c->scratch})
+    if (p) cudaFree(p);
+  delete c;
+}
+
+__global__ void dist_of_kernel(const int32_t* group_off, int G, int n, int32_t* dist_of, int* bad) {
+  for (int g = blockIdx.x; g < G; g += gridDim.x) {
+    const int lo = group_off[g], hi = group_off[g + 1];
+    if (threadIdx.x == 0 && (lo > hi || lo < 0 || hi > n)) atomicAdd(bad, 1);
+    for (int i = lo + threadIdx.x; i < hi && i < n && i >= 0; i += blockDim.x) dist_of[i] = g;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (group_off[0] != 0 || group_off[G] != n))
+    atomicAdd(bad, 1);
+}
+
+int grid_for(int64_t total, int threads) {
+  int64_t b = (total + threads - 1) / threads;
+  return (int)(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
+}
+
+pf_status build_group_tables(pf_ctx* c, cudaStream_t s) {
+  pf::group_tables_kernel<256><<<c->cfg.n_groups, 256, 0, s>>>(c->xbuf, c->cfg.max_len,
+                                                               c->cfg.window, c->gC, c->gS);
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t pf_abi_version(void) { return PF_ABI_VERSION; }
+
+const char* pf_last_error(void) { return g_last_error.c_str(); }
+
+pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* stream,
+                    pf_ctx** out) {
+  if (!cfg || !out) return fail(PF_EINVAL, "pf_create: NULL cfg/out");
+  *out = nullptr;
+  const pf_config& C = *cfg;
+  if (C.n_instances < 1) return fail(PF_EINVAL, "n_instances must be >= 1");
+  if (C.window < 1) return fail(PF_EINVAL, "window must be >= 1");
+  if (C.max_len < 1 || C.max_len > 32767) return fail(PF_ERANGE, "max_len must be in [1, 32767]");
+  if (C.max_input_len < 0) return fail(PF_EINVAL, "max_input_len must be >= 0");
+  if (C.max_entries < 1 || C.max_entries > 4096)
+    return fail(PF_ERANGE, "max_entries must be in [1, 4096]");
+  if (C.repetitions < 1) return fail(PF_EINVAL, "repetitions must be >= 1");
+  if (C.reserved_bp < 0 || C.reserved_bp > 9999) return fail(PF_EINVAL, "reserved_bp must be in [0, 9999]");
+  if (C.mode != PF_MODE_SAMPLE && C.mode != PF_MODE_QUANTILE) return fail(PF_EINVAL, "bad mode");
+  if ((int64_t)C.max_entries * ((int64_t)C.max_input_len + 2LL * C.max_len) >= (1LL << 31))
+    return fail(PF_ERANGE, "max_entries*(max_input_len + 2*max_len) must be < 2^31");
+  if (C.n_groups < 0) return fail(PF_EINVAL, "n_groups must be >= 0");
+  if (C.n_groups > 0) {
+    if (C.window % 8) return fail(PF_EINVAL, "shared mode: window must be a multiple of 8");
+    if (!C.group_off) return fail(PF_EINVAL, "shared mode: group_off required");
+    if (C.nranks < 1 || 8 % C.nranks || C.rank < 0 || C.rank >= C.nranks)
+      return fail(PF_EINVAL, "shared mode: nranks must divide 8 and 0 <= rank < nranks");
+  } else if (C.window > 16384 && C.window <= C.max_len + 1) {
+    return fail(PF_ERANGE, "per-instance window <= Lmax+1 must be <= 16384");
+  }
+  cudaStream_t s = S(stream);
+  pf_ctx* c = new pf_ctx();
+  c->cfg = C;
+  c->cfg.group_off = nullptr;
+  if (C.n_groups > 0) {
+    c->layout = LAYOUT_GROUP;
+    c->shards_owned = 8 / C.nranks;
+    c->n_rows = C.n_groups * c->shards_owned;
+    c->row_window = C.window / 8;
+    c->rows_per_hist = c->shards_owned;
+  } else {
+    c->layout = (C.window <= C.max_len + 1) ? LAYOUT_SORTED : LAYOUT_HIST;
+    c->shards_owned = 1;
+    c->n_rows = C.n_instances;
+    c->row_window = C.window;
+    c->rows_per_hist = 1;
+  }
+  auto cleanup_fail = [&](pf_status st) { free_ctx(c); return st; };
+#define PF_CUDA_C(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      fail(e_ == cudaErrorMemoryAllocation ? PF_ENOMEM : PF_ECUDA, "%s: %s", #call,        \
+           cudaGetErrorString(e_));                                                       \
+      return cleanup_fail(e_ == cudaErrorMemoryAllocation ? PF_ENOMEM : PF_ECUDA);        \
+    }                                                                                     \
+  } while (0)
+  const int64_t ring_elems = (int64_t)c->n_rows * c->row_window;
+  const int nb = C.max_len + 1;
+  PF_CUDA_C(cudaMalloc(&c->ring, ring_elems * 4 + 16));
+  PF_CUDA_C(cudaMalloc(&c->head, (size_t)c->n_rows * 4 + 16));
+  PF_CUDA_C(cudaMalloc(&c->err, 16));
+  PF_CUDA_C(cudaMalloc(&c->scratch, 16));
+  PF_CUDA_C(cudaMemsetAsync(c->head, 0, (size_t)c->n_rows * 4, s));
+  PF_CUDA_C(cudaMemsetAsync(c->err, 0, 16, s));
+  PF_CUDA_C(cudaMemsetAsync(c->scratch, 0, 16, s));
+  pf::init_ring_kernel<<<grid_for(ring_elems, 256), 256, 0, s>>>(c->ring, ring_elems, init_history,
+                                                                  C.max_len, c->scratch);
+  PF_CUDA_C(cudaGetLastError());
+  if (c->layout == LAYOUT_SORTED) {
+    PF_CUDA_C(cudaMalloc(&c->sorted, ring_elems * 4 + 16));
+    int P2 = 1;
+    while (P2 < c->row_window) P2 <<= 1;
+    PF_CUDA_C(cudaFuncSetAttribute(pf::sort_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   P2 * 4));
+    pf::sort_rows_kernel<<<c->n_rows, 512, P2 * 4, s>>>(c->ring, c->sorted, c->row_window, P2);
+    PF_CUDA_C(cudaGetLastError());
+  } else {
+    const int hist_rows = (c->layout == LAYOUT_HIST) ? C.n_instances : C.n_groups;
+    PF_CUDA_C(cudaMalloc(&c->hist, (size_t)hist_rows * nb * 4 + 16));
+    PF_CUDA_C(cudaMemsetAsync(c->hist, 0, (size_t)hist_rows * nb * 4, s));
+    pf::hist_rows_kernel<<<grid_for(ring_elems, 256), 256, 0, s>>>(
+        c->ring, ring_elems, c->row_window, c->rows_per_hist, C.max_len, c->hist);
+    PF_CUDA_C(cudaGetLastError());
+  }
+  if (c->layout == LAYOUT_GROUP) {
+    const int G = C.n_groups;
+    PF_CUDA_C(cudaMalloc(&c->xbuf, (size_t)G * nb * 4 + 16));
+    PF_CUDA_C(cudaMalloc(&c->gC, (size_t)G * nb * 4 + 16));
+    PF_CUDA_C(cudaMalloc(&c->gS, (size_t)G * C.window * 4 + 16));
+    PF_CUDA_C(cudaMalloc(&c->dist_of, (size_t)C.n_instances * 4 + 16));
+    PF_CUDA_C(cudaMalloc(&c->group_off, (size_t)(G + 1) * 4 + 16));
+    PF_CUDA_C(cudaMemcpyAsync(c->group_off, C.group_off, (size_t)(G + 1) * 4,
+                              cudaMemcpyDeviceToDevice, s));
+    dist_of_kernel<<<G, 128, 0, s>>>(c->group_off, G, C.n_instances, c->dist_of, c->scratch);
+    PF_CUDA_C(cudaGetLastError());
+    PF_CUDA_C(cudaMemcpyAsync(c->xbuf, c->hist, (size_t)G * nb * 4, cudaMemcpyDeviceToDevice, s));
+    if (C.nranks == 1) {
+      pf_status st = build_group_tables(c, s);
+      if (st != PF_OK) return cleanup_fail(st);
+    }
+  }
+  int n_bad = 0;
+  PF_CUDA_C(cudaMemcpyAsync(&n_bad, c->scratch, 4, cudaMemcpyDeviceToHost, s));
+  PF_CUDA_C(cudaStreamSynchronize(s));
+  if (n_bad) {
+    fail(PF_EINVAL, "pf_create: %d invalid init_history values / group offsets", n_bad);
+    return cleanup_fail(PF_EINVAL);
+  }
+  // Admit-kernel variant and its shared memory footprint.
+  c->variant = -1;
+  for (int v = 0; v < kNumVariants; ++v)
+    if (kVariants[v].T * kVariants[v].IPT >= C.max_entries) { c->variant = v; break; }
+  const Variant& V = kVariants[c->variant];
+  c->n_bins = 2 * V.T;
+  c->bin_shift = 0;
+  while (((C.max_len - 1) >> c->bin_shift) >= c->n_bins) ++c->bin_shift;
+  size_t table = 0;
+  if (c->layout == LAYOUT_SORTED) table = (size_t)C.window * 4;
+  if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
+  c->admit_smem = (size_t)16 * V.T * V.IPT + (size_t)8 * c->n_bins + 64 * 4 + table;
+  const int look = c->layout;
+  if (c->admit_smem > 227 * 1024) {
+    fail(PF_ERANGE, "admit kernel needs %zu B of shared memory", c->admit_smem);
+    return cleanup_fail(PF_ERANGE);
+  }
+  PF_CUDA_C(cudaFuncSetAttribute(V.fn[look], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)c->admit_smem));
+#undef PF_CUDA_C
+  *out = c;
+  return PF_OK;
+}
+
+pf_status pf_destroy(pf_ctx* ctx) {
+  if (!ctx) return fail(PF_EINVAL, "pf_destroy: NULL ctx");
+  cudaDeviceSynchronize();
+  free_ctx(ctx);
+  return PF_OK;
+}
+
+pf_status pf_update_history(pf_ctx* c, const int32_t* comp_off, const int32_t* comp_len,
+                            int32_t total, void* stream) {
+  if (!c || !comp_off) return fail(PF_EINVAL, "pf_update_history: NULL ctx/comp_off");
+  if (total < 0 || (total > 0 && !comp_len)) return fail(PF_EINVAL, "pf_update_history: bad total/comp_len");
+  cudaStream_t s = S(stream);
+  const int threads = 256;
+  const int blocks = (int)(((int64_t)c->n_rows * 32 + threads - 1) / threads);
+  if (c->layout == LAYOUT_SORTED) {
+    pf::update_sorted_kernel<<<blocks, threads, 0, s>>>(c->n_rows, c->row_window, c->cfg.max_len,
+                                                        comp_off, comp_len, c->ring, c->head,
+                                                        c->sorted, c->err);
+  } else {
+    pf::update_hist_kernel<<<blocks, threads, 0, s>>>(c->n_rows, c->row_window, c->rows_per_hist,
+                                                      c->cfg.max_len, comp_off, comp_len, c->ring,
+                                                      c->head, c->hist, c->err);
+  }
+  PF_CUDA(cudaGetLastError());
+  if (c->layout == LAYOUT_GROUP) {
+    const size_t bytes = (size_t)c->cfg.n_groups * (c->cfg.max_len + 1) * 4;
+    PF_CUDA(cudaMemcpyAsync(c->xbuf, c->hist, bytes, cudaMemcpyDeviceToDevice, s));
+    if (c->cfg.nranks == 1) return build_group_tables(c, s);
+  }
+  return PF_OK;
+}
+
+pf_status pf_exchange_buffer(pf_ctx* c, int32_t** buf, int64_t* count) {
+  if (!c || !buf || !count) return fail(PF_EINVAL, "pf_exchange_buffer: NULL argument");
+  if (c->layout != LAYOUT_GROUP) return fail(PF_ESTATE, "pf_exchange_buffer: not in shared mode");
+  *buf = c->xbuf;
+  *count = (int64_t)c->cfg.n_groups * (c->cfg.max_len + 1);
+  return PF_OK;
+}
+
+pf_status pf_commit_history(pf_ctx* c, void* stream) {
+  if (!c) return fail(PF_EINVAL, "pf_commit_history: NULL ctx");
+  if (c->layout != LAYOUT_GROUP) return PF_OK;
+  return build_group_tables(c, S(stream));
+}
+
+static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* input_len,
+                              const int32_t* generated, const int32_t* q_off,
+                              const int32_t* q_input_len, const int32_t* max_new,
+                              const int32_t* capacity, uint32_t tick, int32_t* admitted_out,
+                              int32_t* peak_out, int32_t* peak_running_out, int32_t* pred_run_out,
+                              int32_t* pred_q_out, cudaStream_t s) {
+  const pf_config& C = c->cfg;
+  pf::AdmitParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = C.n_instances;
+  p.w = C.window;
+  p.max_len = C.max_len;
+  p.max_input_len = C.max_input_len;
+  p.max_entries = C.max_entries;
+  p.mode = C.mode;
+  p.quantile_u = C.quantile_u;
+  p.R = C.repetitions;
+  p.bp = C.reserved_bp;
+  p.seed = C.seed;
+  p.tick = tick;
+  p.instance_base = C.instance_base;
+  p.members_per_group = C.members_per_group;
+  p.member_base = C.member_base;
+  p.bin_shift = c->bin_shift;
+  p.n_bins = c->n_bins;
+  p.sorted = c->sorted;
+  p.hist = c->hist;
+  p.gC = c->gC;
+  p.gS = c->gS;
+  p.dist_of = c->dist_of;
+  p.group_off = c->group_off;
+  p.run_off = run_off;
+  p.input_len = input_len;
+  p.generated = generated;
+  p.q_off = q_off;
+  p.q_input_len = q_input_len;
+  p.max_new = max_new;
+  p.capacity = capacity;
+  p.admitted_out = admitted_out;
+  p.peak_out = peak_out;
+  p.peak_running_out = peak_running_out;
+  p.pred_run_out = pred_run_out;
+  p.pred_q_out = pred_q_out;
+  p.err = c->err;
+  const Variant& V = kVariants[c->variant];
+  V.fn[c->layout]<<<C.n_instances, V.T, c->admit_smem, s>>>(p);
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+pf_status pf_estimate_peak(pf_ctx* c, const int32_t* run_off, const int32_t* input_len,
+                           const int32_t* generated, const int32_t* max_new, uint32_t tick,
+                           int32_t* peak_out, int32_t* pred_out, void* stream) {
+  if (!c || !run_off || !input_len || !generated || !max_new || !peak_out)
+    return fail(PF_EINVAL, "pf_estimate_peak: NULL required pointer");
+  return launch_admit(c, run_off, input_len, generated, nullptr, nullptr, max_new, nullptr, tick,
+                      nullptr, peak_out, nullptr, pred_out, nullptr, S(stream));
+}
+
+pf_status pf_admit(pf_ctx* c, const int32_t* run_off, const int32_t* input_len,
+                   const int32_t* generated, const int32_t* q_off, const int32_t* q_input_len,
+                   const int32_t* max_new, const int32_t* capacity, uint32_t tick,
+                   int32_t* admitted_out, int32_t* peak_out, int32_t* peak_running_out,
+                   int32_t* pred_run_out, int32_t* pred_q_out, void* stream) {
+  if (!c || !run_off || !input_len || !generated || !q_off || !q_input_len || !max_new ||
+      !capacity || !admitted_out || !peak_out)
+    return fail(PF_EINVAL, "pf_admit: NULL required pointer");
+  return launch_admit(c, run_off, input_len, generated, q_off, q_input_len, max_new, capacity,
+                      tick, admitted_out, peak_out, peak_running_out, pred_run_out, pred_q_out,
+                      S(stream));
+}
+
+pf_status pf_get_device_error(pf_ctx* c, int32_t* code, int32_t* index, void* stream) {
+  if (!c || !code || !index) return fail(PF_EINVAL, "pf_get_device_error: NULL argument");
+  int host[2] = {0, 0};
+  PF_CUDA(cudaMemcpyAsync(host, c->err, 8, cudaMemcpyDeviceToHost, S(stream)));
+  PF_CUDA(cudaStreamSynchronize(S(stream)));
+  *code = host[0];
+  *index = host[1];
+  return PF_OK;
+}
+
+pf_status pf_clear_device_error(pf_ctx* c, void* stream) {
+  if (!c) return fail(PF_EINVAL, "pf_clear_device_error: NULL ctx");
+  PF_CUDA(cudaMemsetAsync(c->err, 0, 8, S(stream)));
+  return PF_OK;
+}
+
+pf_status pf_export_history(pf_ctx* c, int32_t* rows_out, void* stream) {
+  if (!c || !rows_out) return fail(PF_EINVAL, "pf_export_history: NULL argument");
+  const int64_t total = (int64_t)c->n_rows * c->row_window;
+  pf::export_rows_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(c->ring, c->head, c->n_rows,
+                                                                       c->row_window, rows_out);
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+}  // extern "C"

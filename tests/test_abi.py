@@ -1,0 +1,69 @@
+"""The C-ABI library loads and exports every symbol include/pfsched.h declares, and
+host-checkable argument errors return synchronously (no GPU needed for these)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "pfsched.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pf_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2507_10150_b200 import build
+    build.build()
+    import paper_2507_10150_b200 as P
+    return P.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    decl = _declared()
+    assert {"pf_create", "pf_destroy", "pf_update_history", "pf_estimate_peak", "pf_admit"} <= set(decl)
+    for name in decl:
+        assert hasattr(lib, name), name
+    import paper_2507_10150_b200 as P
+    assert set(P.SYMBOLS) == set(decl)
+
+
+def test_abi_version(lib):
+    assert lib.pf_abi_version() == 1
+
+
+def _cfg(**kw):
+    from paper_2507_10150_b200.binding import PFConfig
+    base = dict(n_instances=4, window=100, max_len=512, max_input_len=512, max_entries=64, n_groups=0,
+                group_off=None, instance_base=0, members_per_group=0, member_base=0, mode=0,
+                quantile_u=0, repetitions=1, reserved_bp=0, seed=0, rank=0, nranks=1)
+    base.update(kw)
+    return PFConfig(**base)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(n_instances=0), -1), (dict(window=0), -1), (dict(max_len=0), -2), (dict(max_len=40000), -2),
+    (dict(max_entries=5000), -2), (dict(repetitions=0), -1), (dict(reserved_bp=10000), -1),
+    (dict(mode=7), -1), (dict(max_input_len=10**7, max_entries=4096), -2),
+    (dict(n_groups=2, window=100), -1), (dict(n_groups=2, window=96), -1),
+    (dict(n_groups=2, window=96, group_off=1234, nranks=3), -1),
+])
+def test_host_validation(lib, kw, status):
+    h = ctypes.c_void_p()
+    cfg = _cfg(**kw)
+    st = lib.pf_create(ctypes.byref(cfg), None, None, ctypes.byref(h))
+    assert st == status
+    assert h.value is None
+    assert len(lib.pf_last_error()) > 0
+
+
+def test_null_arguments(lib):
+    assert lib.pf_create(None, None, None, None) == -1
+    assert lib.pf_destroy(None) == -1
+    assert lib.pf_admit(*([None] * 8), 0, *([None] * 6)) == -1
+    assert lib.pf_estimate_peak(None, None, None, None, None, 0, None, None, None) == -1
+    assert lib.pf_update_history(None, None, None, 0, None) == -1
