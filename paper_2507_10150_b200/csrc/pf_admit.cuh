@@ -1,9 +1,30 @@
 // pf_admit.cuh — the fused per-instance hot-path kernel of libpfsched (sm_100a):
 //   a3/a4  distribution lookup + conditional quantile  (Eq.(eq:5), Alg.1 l.3-9)
-//   a5     segmented sort by remaining length r desc     (Eq.(eq:1))
-//   a6     scan + max: M_i = Σ_{j≤i} a_j + r_i·i, M*     (Eq.(eq:2)-(eq:3))
+//   a5/a6  future required memory M* (Eq.(eq:1)-(eq:3)) — sort-free, see below
 //   a7     prefix-admission search over the FIFO queue   (Alg.1 l.7-14)
-// One CTA per instance; every step runs on-chip (shared memory + registers).
+//
+// Mapping: a TEAM of TW warps owns one instance (TW = 1 for ≤ 512 requests per
+// instance: every sync is a __syncwarp, every scan a warp shuffle scan); several
+// teams share a CTA. Everything after the input loads runs on-chip.
+//
+// M* without sorting. Eq.(eq:1)-(eq:3) equal the tick form
+//   M* = max_τ T(τ),  T(τ) = Σ_{e: r_e ≥ τ} (a_e + τ),
+// whose maximum sits at some r_e. Requests are binned by r with a monotone map
+// (bin 0 = largest r; width-1 bins for r ≤ 16, 8 bins per octave up to width 2^s,
+// then width 2^s; 128 bins per warp). With A_b, N_b the sums of a and counts over bins 0..b, and
+// [lo_b, hi_b] the r-range of bin b:
+//   T(lo_b) = A_b + lo_b·N_b                 exactly (a valid lower bound L of M*);
+//   T(τ) ≤ A_b + hi_b·N_b for τ ∈ [lo_b, hi_b] (an upper bound U_b).
+// Width-1 bins are exact. A wide non-empty bin can only hold the maximum if U_b > L;
+// those rare bins (≈0.9 per evaluation on the paper-shaped workloads) are refined
+// exactly from their members. This equals the sorted form bit for bit and costs
+// O(bins + requests) with no sort.
+//
+// a7 is a cutting-plane search that returns exactly Alg.1's p* (DESIGN.md §6):
+// T_p(τ) (with queue prefix 1..p) is non-decreasing in p for every τ, so M*(p) is
+// too. From p̂ = q, take τ* with T_p̂(τ*) = M*(p̂) > C and jump to p̂ ← p_max(τ*) =
+// the largest p with T_p(τ*) ≤ C (one FIFO prefix scan). Every p > p_max(τ*)
+// violates at τ*, so p* ≤ p̂ always; stop when M*(p̂) ≤ C, i.e. p̂ = p*.
 #pragma once
 #include "pf_common.cuh"
 
@@ -25,8 +46,10 @@ struct AdmitParams {
   uint32_t tick;
   int64_t instance_base;
   int members_per_group, member_base;
-  int bin_shift;       // coarse bin = (Lmax - r) >> bin_shift
-  int n_bins;
+  int team_smem;       // bytes of shared memory per team
+  int ent_cap;         // request slots per team (>= max_entries)
+  const uint16_t* bintab;  // [Lmax+1]: r -> bin
+  const uint32_t* edges;   // [n_bins]: lo | hi << 16 (0 = no r maps to the bin)
   // history tables
   const int32_t* sorted;     // LOOK_SORTED [n × w]
   const int32_t* hist;       // LOOK_HIST   [n × (Lmax+1)]
@@ -51,14 +74,6 @@ struct AdmitParams {
   int32_t* err;
 };
 
-// Packed entry: r (15 bits) << 48 | j (16 bits) << 32 | a (31 bits).
-__device__ __forceinline__ uint64_t pack_entry(int r, int j, int a) {
-  return ((uint64_t)(uint32_t)r << 48) | ((uint64_t)(uint32_t)j << 32) | (uint32_t)a;
-}
-__device__ __forceinline__ int ent_r(uint64_t e) { return (int)(e >> 48); }
-__device__ __forceinline__ int ent_j(uint64_t e) { return (int)((e >> 32) & 0xFFFF); }
-__device__ __forceinline__ int ent_a(uint64_t e) { return (int)(e & 0xFFFFFFFFu); }
-
 // #{x in S[0..w) : x <= v} for ascending S (upper_bound).
 __device__ __forceinline__ int upper_bound_smem(const int32_t* S, int w, int v) {
   int lo = 0, len = w;
@@ -71,29 +86,140 @@ __device__ __forceinline__ int upper_bound_smem(const int32_t* S, int w, int v) 
   return lo;
 }
 
-// 10^4·M ≤ (10^4 − bp)·cap  (C-12, C-13), exact in int64.
-__device__ __forceinline__ bool fits(int m, int cap, int bp) {
-  return (int64_t)m * 10000 <= (int64_t)(10000 - bp) * (int64_t)cap;
-}
+// ---------------------------------------------------------------- team primitives
+template <int TW>
+struct Team {
+  static constexpr int TT = TW * 32;
+  int tid, lane, wid, id;
+  int* xs;  // team scratch: [0, 4·TW) reductions, [120, 122) pick
+  __device__ __forceinline__ void sync() const {
+    if constexpr (TW == 1) {
+      __syncwarp();
+    } else {
+      asm volatile("bar.sync %0, %1;" ::"r"(id + 1), "r"(TT) : "memory");
+    }
+  }
+  // exclusive prefix (in team thread order) of NV values; totals in tot.
+  template <int NV>
+  __device__ __forceinline__ void excl(int (&v)[NV], int (&tot)[NV]) const {
+    int inc[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) inc[c] = warp_inclusive_add(v[c], lane);
+    if constexpr (TW == 1) {
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        tot[c] = __shfl_sync(0xffffffffu, inc[c], 31);
+        v[c] = inc[c] - v[c];
+      }
+    } else {
+      if (lane == 31) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) xs[c * TW + wid] = inc[c];
+      }
+      sync();
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        int base = 0, total = 0;
+#pragma unroll
+        for (int x = 0; x < TW; ++x) {
+          const int s = xs[c * TW + x];
+          base += (x < wid) ? s : 0;
+          total += s;
+        }
+        v[c] = base + inc[c] - v[c];
+        tot[c] = total;
+      }
+      sync();
+    }
+  }
+  __device__ __forceinline__ int max(int v) const {
+    v = __reduce_max_sync(0xffffffffu, v);
+    if constexpr (TW == 1) {
+      return v;
+    } else {
+      if (lane == 0) xs[wid] = v;
+      sync();
+      int m = xs[0];
+#pragma unroll
+      for (int x = 1; x < TW; ++x) m = ::max(m, xs[x]);
+      sync();
+      return m;
+    }
+  }
+  __device__ __forceinline__ bool any(bool b) const {
+    if constexpr (TW == 1) {
+      return __any_sync(0xffffffffu, b);
+    } else {
+      return this->max(b ? 1 : 0) != 0;
+    }
+  }
+  // (v1, v2) of the lowest thread with own == true (team-uniform result).
+  __device__ __forceinline__ void pick(bool own, int& v1, int& v2) const {
+    if constexpr (TW == 1) {
+      const int who = __ffs(__ballot_sync(0xffffffffu, own)) - 1;
+      v1 = __shfl_sync(0xffffffffu, v1, who);
+      v2 = __shfl_sync(0xffffffffu, v2, who);
+    } else {
+      const int who = -this->max(own ? -tid : -(1 << 20));
+      if (tid == who) {  // xs[120..121]: between the candidate and member lists
+        xs[120] = v1;
+        xs[121] = v2;
+      }
+      sync();
+      v1 = xs[120];
+      v2 = xs[121];
+      sync();
+    }
+  }
+};
 
-// Dynamic shared memory layout (bytes):
-//   [0, 16·E)            ent_tmp (E = T·IPT packed entries) then ent_sorted
-//   next 2·NB·4          bin counts, bin starts
-//   next 64·4            scan scratch
-//   next table           S[w] (LOOK_SORTED) | C[Lmax+1] (LOOK_HIST) | none
-template <int T, int IPT, int LOOK>
-__global__ void __launch_bounds__(T) admit_kernel(AdmitParams p) {
-  constexpr int E = T * IPT;
+// Result of one M* evaluation over R ∪ Q' (Q' = the queue entries currently in binQ).
+struct Eval {
+  int m_run;   // max_τ T_R(τ)           (running requests only)
+  int m_all;   // max_τ T_{R∪Q'}(τ)
+  int tau;     // a τ attaining m_all
+  int t_run;   // T_R(tau)
+};
+
+// Per-team shared memory layout (bytes, in order):
+//   rb[ent_cap] u32  (r | bin << 16, original request order: e < k running, then queue)
+//   av[ent_cap] u32  (a = l_p + l_t)
+//   binR[NBW] u32, binQ[NBW] u32: per-bin (A, N) — packed A << 9 | N when PACK, else
+//                    A in [0, NB) and N in [NB, 2·NB)
+//   xs[256] i32      scratch: reductions, candidate list, member list
+//   table            S[w] (LOOK_SORTED) | C[Lmax+1] (LOOK_HIST)
+// CTA prefix: edges[NB] u32 shared by the teams.
+template <int TW, int LOOK, bool PACK>
+__global__ void __launch_bounds__((TW == 1 ? 4 : 1) * TW * 32, (TW == 1 ? 8 : 2))
+admit_kernel(AdmitParams p) {
+  constexpr int TT = TW * 32;
+  constexpr int TEAMS = (TW == 1) ? 4 : 1;
+  constexpr int NB = 128 * TW;  // 4 bins per thread
+  constexpr int BPT = 4;
+  constexpr int NBW = PACK ? NB : 2 * NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* ent_tmp = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* ent_sorted = ent_tmp + E;
-  int* bin_cnt = reinterpret_cast<int*>(ent_sorted + E);
-  int* bin_start = bin_cnt + p.n_bins;
-  int* scratch = bin_start + p.n_bins;
-  int32_t* table = scratch + 64;
+  uint32_t* edges = reinterpret_cast<uint32_t*>(smem_raw);
+  for (int b = threadIdx.x; b < NB; b += TEAMS * TT) edges[b] = __ldg(p.edges + b);
+  __syncthreads();
 
-  const int i = blockIdx.x;
-  const int tid = threadIdx.x;
+  Team<TW> T;
+  T.id = threadIdx.x / TT;
+  T.tid = threadIdx.x % TT;
+  T.lane = threadIdx.x & 31;
+  T.wid = T.tid >> 5;
+  unsigned char* base = smem_raw + NB * 4 + (size_t)T.id * p.team_smem;
+  uint32_t* rb = reinterpret_cast<uint32_t*>(base);
+  int* av = reinterpret_cast<int*>(rb + p.ent_cap);
+  uint32_t* binR = reinterpret_cast<uint32_t*>(av + p.ent_cap);
+  uint32_t* binQ = binR + NBW;
+  T.xs = reinterpret_cast<int*>(binQ + NBW);
+  int* cand = T.xs + 32;    // [0]: count, then 5 ints per candidate (≤ 16)
+  int* memb = T.xs + 128;   // [0]: count, then (r, a, is_run) per member (≤ 40)
+  int32_t* table = T.xs + 256;
+
+  const int i = blockIdx.x * TEAMS + T.id;
+  if (i >= p.n) return;
+  const int tid = T.tid;
   const bool estimate_only = (p.q_off == nullptr);
 
   // ---- instance scalars and CSR validation
@@ -115,16 +241,18 @@ __global__ void __launch_bounds__(T) admit_kernel(AdmitParams p) {
       if (p.peak_running_out) p.peak_running_out[i] = -1;
     }
     if (bad != PF_BAD_OFFSETS) {
-      for (int e = tid; e < k; e += T)
-        if (p.pred_run_out) p.pred_run_out[r0 + e] = -1;
-      for (int e = tid; e < q; e += T)
-        if (p.pred_q_out) p.pred_q_out[q0 + e] = -1;
+      if (p.pred_run_out)
+        for (int e = tid; e < k; e += TT) p.pred_run_out[r0 + e] = -1;
+      if (p.pred_q_out)
+        for (int e = tid; e < q; e += TT) p.pred_q_out[q0 + e] = -1;
     }
     return;
   }
+  // C = the largest integer M* that fits: 10^4·M* ≤ (10^4 − bp)·cap (C-12, C-13).
+  const int Cmax = estimate_only ? 0 : (int)(((int64_t)(10000 - p.bp) * cap) / 10000);
 
   // ---- a3: the distribution P(l) of Eq.(eq:5) as a lookup structure
-  int w = p.w;
+  const int w = p.w;
   const int32_t* gC = nullptr;
   const int32_t* gS = nullptr;
   int64_t gid;
@@ -136,105 +264,124 @@ __global__ void __launch_bounds__(T) admit_kernel(AdmitParams p) {
   } else {
     gid = p.instance_base + i;
   }
-  for (int b = tid; b < p.n_bins; b += T) bin_cnt[b] = 0;
+  {
+    uint4* z4 = reinterpret_cast<uint4*>(binR);  // binR and binQ are contiguous
+#pragma unroll
+    for (int x = 0; x < 2 * NBW / 4 / TT; ++x) z4[tid + x * TT] = make_uint4(0, 0, 0, 0);
+  }
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
-    for (int x = tid; x < w; x += T) table[x] = __ldg(src + x);
+    for (int x = tid; x < w; x += TT) table[x] = __ldg(src + x);
   } else if (LOOK == LOOK_HIST) {
     // C[l] = #{h ∈ L_h : h ≤ l}: inclusive scan of the persistent histogram.
     const int nb = p.max_len + 1;
     const int32_t* src = p.hist + (int64_t)i * nb;
-    const int per = (nb + T - 1) / T;
-    int run = 0;
-    const int lo = tid * per;
-    for (int x = lo; x < min(nb, lo + per); ++x) run += __ldg(src + x);
-    int v[1] = {run}, tot[1];
-    block_exclusive_add<T, 1>(v, tot, scratch);
-    int acc = v[0];
-    for (int x = lo; x < min(nb, lo + per); ++x) {
-      acc += __ldg(src + x);
-      table[x] = acc;
+    int carry = 0;
+    for (int x0 = 0; x0 < nb; x0 += TT) {
+      const int x = x0 + tid;
+      int v[1] = {x < nb ? __ldg(src + x) : 0}, tot[1];
+      const int own = v[0];
+      T.template excl<1>(v, tot);
+      if (x < nb) table[x] = carry + v[0] + own;
+      carry += tot[0];
     }
   }
-  __syncthreads();
+  T.sync();
 
-  // ---- a4: predictions (Alg.1 lines 3-9), then (r, a, j) and coarse bins
+  // ---- a4: predictions (Alg.1 lines 3-9), 4 requests per thread per chunk with the
+  // chunk's loads issued together; each request's (a, 1) is added to its r-bin.
   uint32_t key_fold = 0;
   if (p.mode == 0) {
     const uint64_t K = instance_key(p.seed, p.tick, gid);
     key_fold = (uint32_t)K ^ (uint32_t)(K >> 32);
   }
-  uint64_t item[IPT];
-  int item_bin[IPT], item_slot[IPT];
+  const int m_used = (n_ent + TT - 1) / TT;
+  const bool want_pred = (p.pred_run_out != nullptr) || (p.pred_q_out != nullptr);
   int my_bad = 0;
+#pragma unroll 1
+  for (int m0 = 0; m0 < m_used; m0 += 4) {
+    int lp[4], lt[4], bq[4], lh[4];
+    uint32_t u[4];
 #pragma unroll
-  for (int m = 0; m < IPT; ++m) {
-    const int e = tid + m * T;
-    item[m] = 0;
-    item_bin[m] = -1;
-    if (e < n_ent) {
-      int l_p, l_t, j;
-      if (e < k) {
-        l_p = p.input_len[r0 + e];
-        l_t = p.generated[r0 + e];
-        j = 0;
+    for (int c = 0; c < 4; ++c) {
+      const int e = tid + (m0 + c) * TT;
+      const bool run = e < k;
+      const int32_t* src = run ? p.input_len + r0 + e : p.q_input_len + (q0 - k) + e;
+      lp[c] = (e < n_ent) ? __ldg(src) : 0;
+      lt[c] = run ? __ldg(p.generated + r0 + e) : 0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int e = tid + (m0 + c) * TT;
+      // l_p ∉ [0, max_input_len] or l_t ∉ [0, max_new) (unsigned compares catch < 0)
+      my_bad |= (e < n_ent) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
+                               ((unsigned)lt[c] >= (unsigned)max_new));
+      lt[c] = ::min(::max(lt[c], 0), max_new - 1);  // keep lookups in range; outputs dropped if bad
+      if (p.mode != 0) u[c] = p.quantile_u;
+      else if (p.R == 1) u[c] = lowbias32(key_fold ^ ((uint32_t)e * 0x9E3779B9U));
+      else u[c] = draw_u(key_fold, e, p.R);
+      if (LOOK == LOOK_GROUP) bq[c] = __ldg(gC + lt[c]);
+      else if (LOOK == LOOK_HIST) bq[c] = table[lt[c]];
+      else bq[c] = upper_bound_smem(table, w, lt[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int n_gt = w - bq[c];
+      const int x = bq[c] + (int)__umulhi(u[c], (uint32_t)n_gt);
+      if (LOOK == LOOK_GROUP) {
+        lh[c] = n_gt ? __ldg(gS + x) : max_new;
+      } else if (LOOK == LOOK_SORTED) {
+        lh[c] = n_gt ? table[x] : max_new;
       } else {
-        l_p = p.q_input_len[q0 + (e - k)];
-        l_t = 0;
-        j = e - k + 1;
-      }
-      if (l_p < 0 || l_p > p.max_input_len) my_bad = my_bad ? my_bad : PF_BAD_INPUT_LEN;
-      if (l_t < 0 || l_t >= max_new) my_bad = my_bad ? my_bad : PF_BAD_GENERATED;
-      l_t = min(max(l_t, 0), max_new - 1);  // keep lookups in range; outputs are discarded if bad
-      const uint32_t u = (p.mode == 0) ? draw_u(key_fold, e, p.R) : p.quantile_u;
-      int l_hat;
-      if (LOOK == LOOK_SORTED) {
-        const int base = upper_bound_smem(table, w, l_t);
-        const int n_gt = w - base;
-        l_hat = n_gt ? table[base + (int)__umulhi(u, (uint32_t)n_gt)] : max_new;
-      } else if (LOOK == LOOK_HIST) {
-        const int base = table[l_t];
-        const int n_gt = w - base;
-        if (n_gt == 0) {
-          l_hat = max_new;
-        } else {
-          const int target = base + (int)__umulhi(u, (uint32_t)n_gt);
-          int lo = l_t + 1, len = p.max_len - l_t;  // smallest L with C[L] > target
-          while (len > 0) {
-            int half = len >> 1;
-            bool right = table[lo + half] <= target;
-            lo = right ? lo + half + 1 : lo;
-            len = right ? len - half - 1 : half;
-          }
-          l_hat = lo;
+        int lo = lt[c] + 1, len = n_gt ? p.max_len - lt[c] : 0;  // smallest L with C[L] > x
+        while (len > 0) {
+          const int half = len >> 1;
+          const bool right = table[lo + half] <= x;
+          lo = right ? lo + half + 1 : lo;
+          len = right ? len - half - 1 : half;
         }
-      } else {
-        const int base = __ldg(gC + l_t);
-        const int n_gt = w - base;
-        l_hat = n_gt ? __ldg(gS + base + (int)__umulhi(u, (uint32_t)n_gt)) : max_new;
+        lh[c] = n_gt ? lo : max_new;
       }
-      l_hat = min(l_hat, max_new);
-      if (e < k) {
-        if (p.pred_run_out) p.pred_run_out[r0 + e] = l_hat;
-      } else {
-        if (p.pred_q_out) p.pred_q_out[q0 + (e - k)] = l_hat;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int e = tid + (m0 + c) * TT;
+      if (e < n_ent) {
+        const int l_hat = ::min(lh[c], max_new);
+        const bool run = e < k;
+        if (want_pred) {
+          int32_t* pout = run ? p.pred_run_out : p.pred_q_out;
+          if (pout) pout[run ? r0 + e : q0 - k + e] = l_hat;
+        }
+        const int r = l_hat - lt[c];  // ≥ 1 (C-4)
+        const int a = lp[c] + lt[c];
+        const int b = __ldg(p.bintab + r);
+        rb[e] = (uint32_t)r | ((uint32_t)b << 16);
+        av[e] = a;
+        uint32_t* bins = run ? binR : binQ;
+        if (PACK) {
+          atomicAdd(&bins[b], ((uint32_t)a << 9) | 1u);
+        } else {
+          atomicAdd(&bins[b], (uint32_t)a);
+          atomicAdd(&bins[NB + b], 1u);
+        }
       }
-      const int r = l_hat - l_t;  // ≥ 1
-      const int a = l_p + l_t;
-      item[m] = pack_entry(r, j, a);
-      const int b = (p.max_len - r) >> p.bin_shift;  // descending r -> ascending bin
-      item_bin[m] = b;
-      item_slot[m] = atomicAdd(&bin_cnt[b], 1);
     }
   }
-  if (__syncthreads_or(my_bad)) {
+  if (T.any(my_bad != 0)) {
     // Data-dependent violation: outputs of this instance are −1.
-    if (my_bad) raise_error(p.err, my_bad, i);
-#pragma unroll
-    for (int m = 0; m < IPT; ++m) {
-      const int e = tid + m * T;
-      if (e < k && p.pred_run_out) p.pred_run_out[r0 + e] = -1;
-      if (e >= k && e < n_ent && p.pred_q_out) p.pred_q_out[q0 + (e - k)] = -1;
+    for (int e = tid; e < n_ent; e += TT) {
+      const int l_p = e < k ? p.input_len[r0 + e] : p.q_input_len[q0 + (e - k)];
+      const int l_t = e < k ? p.generated[r0 + e] : 0;
+      if (l_p < 0 || l_p > p.max_input_len) raise_error(p.err, PF_BAD_INPUT_LEN, i);
+      else if (l_t < 0 || l_t >= max_new) raise_error(p.err, PF_BAD_GENERATED, i);
+    }
+    for (int e = tid; e < n_ent; e += TT) {
+      if (e < k) {
+        if (p.pred_run_out) p.pred_run_out[r0 + e] = -1;
+      } else if (p.pred_q_out) {
+        p.pred_q_out[q0 + (e - k)] = -1;
+      }
     }
     if (tid == 0) {
       if (!estimate_only) p.admitted_out[i] = -1;
@@ -243,131 +390,282 @@ __global__ void __launch_bounds__(T) admit_kernel(AdmitParams p) {
     }
     return;
   }
+  T.sync();
 
-  // ---- a5: segmented sort by r descending — coarse counting pass, then exact
-  // rank inside each bin (ties are irrelevant to every output, C-11).
-  {
-    const int per = (p.n_bins + T - 1) / T;
-    const int lo = tid * per, hi = min(p.n_bins, lo + per);
-    int s = 0;
-    for (int b = lo; b < hi; ++b) s += bin_cnt[b];
-    int v[1] = {s}, tot[1];
-    block_exclusive_add<T, 1>(v, tot, scratch);
-    int acc = v[0];
-    for (int b = lo; b < hi; ++b) {
-      bin_start[b] = acc;
-      acc += bin_cnt[b];
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int m = 0; m < IPT; ++m)
-    if (item_bin[m] >= 0) ent_tmp[bin_start[item_bin[m]] + item_slot[m]] = item[m];
-  __syncthreads();
-#pragma unroll
-  for (int m = 0; m < IPT; ++m) {
-    if (item_bin[m] < 0) continue;
-    const int x = bin_start[item_bin[m]] + item_slot[m];
-    const int lo = bin_start[item_bin[m]], hi = lo + bin_cnt[item_bin[m]];
-    const int rv = ent_r(item[m]);
-    int rank = 0;
-    for (int y = lo; y < hi; ++y) {
-      const int ry = ent_r(ent_tmp[y]);
-      rank += (ry > rv) || (ry == rv && y < x);
-    }
-    ent_sorted[lo + rank] = item[m];
-  }
-  __syncthreads();
-
-  // ---- a6: blocked scan over the sorted order. Keep (r, j, a) in registers.
-  int rr[IPT], jj[IPT], aa[IPT];
-  int sA_R = 0, sN_R = 0, sA = 0, sN = 0;
-#pragma unroll
-  for (int m = 0; m < IPT; ++m) {
-    const int pos = tid * IPT + m;
-    if (pos < n_ent) {
-      const uint64_t e = ent_sorted[pos];
-      rr[m] = ent_r(e);
-      jj[m] = ent_j(e);
-      aa[m] = ent_a(e);
+  // ---- a5/a6: one M* evaluation over R ∪ Q' (Q' = the queue requests in binQ, with
+  // queue position ≤ qlim), header comment. Thread t owns bins [4t, 4t+4).
+  auto bin_an = [&](const uint32_t* bins, int b, int& A, int& N) {
+    if (PACK) {
+      const uint32_t x = bins[b];
+      A = (int)(x >> 9);
+      N = (int)(x & 511u);
     } else {
-      rr[m] = 0;
-      jj[m] = 0x7FFF;  // never included
-      aa[m] = 0;
+      A = (int)bins[b];
+      N = (int)bins[NB + b];
     }
-    const bool in = pos < n_ent;
-    const bool run = in && jj[m] == 0;
-    sA_R += run ? aa[m] : 0;
-    sN_R += run ? 1 : 0;
-    sA += in ? aa[m] : 0;
-    sN += in ? 1 : 0;
-  }
-  int v4[4] = {sA_R, sN_R, sA, sN}, t4[4];
-  block_exclusive_add<T, 4>(v4, t4, scratch);
-  int m0 = 0, mq = 0;
-  {
-    int A_R = v4[0], N_R = v4[1], A = v4[2], N = v4[3];
+  };
+  auto evaluate = [&](int qlim) -> Eval {
+    const int b0 = tid * BPT;
+    int s[4] = {0, 0, 0, 0}, tot[4];
 #pragma unroll
-    for (int m = 0; m < IPT; ++m) {
-      const int pos = tid * IPT + m;
-      if (pos < n_ent) {
-        const bool run = jj[m] == 0;
-        A_R += run ? aa[m] : 0;
-        N_R += run ? 1 : 0;
-        A += aa[m];
-        N += 1;
-        m0 = max(m0, A_R + rr[m] * N_R);  // M_i of Eq.(eq:2), running batch only
-        mq = max(mq, A + rr[m] * N);      // with the whole queue
+    for (int x = 0; x < BPT; ++x) {
+      int A, N, Aq, Nq;
+      bin_an(binR, b0 + x, A, N);
+      bin_an(binQ, b0 + x, Aq, Nq);
+      s[0] += A;
+      s[1] += N;
+      s[2] += Aq;
+      s[3] += Nq;
+    }
+    T.template excl<4>(s, tot);
+    const int s0[4] = {s[0], s[1], s[2], s[3]};
+    // walk: exact T at lower edges (lower bounds), upper bounds of wide bins
+    int lb_r = 0, lb_a = 0, lb_tau = 0, lb_trun = 0, ub_r = 0, ub_a = 0;
+#pragma unroll
+    for (int x = 0; x < BPT; ++x) {
+      int A, N, Aq, Nq;
+      bin_an(binR, b0 + x, A, N);
+      bin_an(binQ, b0 + x, Aq, Nq);
+      s[0] += A;
+      s[1] += N;
+      s[2] += Aq;
+      s[3] += Nq;
+      const uint32_t ed = edges[b0 + x];
+      const int lo = (int)(ed & 0xFFFF), hi = (int)(ed >> 16);
+      const int vr = s[0] + lo * s[1];                    // T_R(lo)
+      const int va = s[0] + s[2] + lo * (s[1] + s[3]);    // T_{R∪Q'}(lo)
+      lb_r = ::max(lb_r, vr);
+      if (va > lb_a) {
+        lb_a = va;
+        lb_tau = lo;
+        lb_trun = vr;
+      }
+      if (hi > lo) {  // wide bin: upper bounds where it holds requests
+        if (N > 0) ub_r = ::max(ub_r, s[0] + hi * s[1]);
+        if (N + Nq > 0) ub_a = ::max(ub_a, s[0] + s[2] + hi * (s[1] + s[3]));
       }
     }
-  }
-  const int M0 = block_max<T>(m0, scratch);  // Eq.(eq:3): M*(R)
-  if (estimate_only) {
-    if (tid == 0) p.peak_out[i] = M0;
-    return;
-  }
-  const int Mq = block_max<T>(mq, scratch);
-
-  // ---- a7: largest FIFO prefix that fits (Alg.1 lines 7-14). M*(p) is monotone
-  // in p, so a binary search over p equals the sequential loop with early return.
-  int p_star, peak;
-  if (q == 0 || !fits(M0, cap, p.bp)) {
-    p_star = 0;
-    peak = M0;
-  } else if (fits(Mq, cap, p.bp)) {
-    p_star = q;
-    peak = Mq;
-  } else {
-    int lo = 0, hi = q, m_lo = M0;  // fits(lo), !fits(hi)
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      int s2[2] = {0, 0};
-#pragma unroll
-      for (int m = 0; m < IPT; ++m) {
-        const bool in = jj[m] <= mid;
-        s2[0] += in ? aa[m] : 0;
-        s2[1] += in ? 1 : 0;
+    Eval ev;
+    ev.m_run = T.max(lb_r);
+    ev.m_all = T.max(lb_a);
+    ev.tau = lb_tau;
+    ev.t_run = lb_trun;
+    T.pick(lb_a == ev.m_all, ev.tau, ev.t_run);
+    const bool need_r = T.max(ub_r) > ev.m_run;
+    const bool need_a = T.max(ub_a) > ev.m_all;
+    if (!need_r && !need_a) return ev;
+    // ---- refinement of the wide bins whose upper bound beats the current maximum
+    if (tid == 0) cand[0] = 0;
+    T.sync();
+    s[0] = s0[0];
+    s[1] = s0[1];
+    s[2] = s0[2];
+    s[3] = s0[3];
+#pragma unroll 1
+    for (int x = 0; x < BPT; ++x) {
+      int A, N, Aq, Nq;
+      bin_an(binR, b0 + x, A, N);
+      bin_an(binQ, b0 + x, Aq, Nq);
+      const uint32_t ed = edges[b0 + x];
+      const int lo = (int)(ed & 0xFFFF), hi = (int)(ed >> 16);
+      const bool c_r = need_r && N > 0 && hi > lo && s[0] + A + hi * (s[1] + N) > ev.m_run;
+      const bool c_a = need_a && N + Nq > 0 && hi > lo &&
+                       s[0] + A + s[2] + Aq + hi * (s[1] + N + s[3] + Nq) > ev.m_all;
+      if (c_r || c_a) {
+        const int slot = atomicAdd(&cand[0], 1);
+        if (slot < 16) {
+          int* cd = cand + 1 + 5 * slot;
+          cd[0] = b0 + x;
+          cd[1] = s[0];  // A_R, N_R, A_Q', N_Q' over the bins before b
+          cd[2] = s[1];
+          cd[3] = s[2];
+          cd[4] = s[3];
+        }
       }
-      int t2[2];
-      block_exclusive_add<T, 2>(s2, t2, scratch);
-      int A = s2[0], N = s2[1], mx = 0;
-#pragma unroll
-      for (int m = 0; m < IPT; ++m) {
-        const bool in = jj[m] <= mid;
-        A += in ? aa[m] : 0;
-        N += in ? 1 : 0;
-        mx = max(mx, A + rr[m] * N);
-      }
-      const int M = block_max<T>(mx, scratch);
-      if (fits(M, cap, p.bp)) {
-        lo = mid;
-        m_lo = M;
+      s[0] += A;
+      s[1] += N;
+      s[2] += Aq;
+      s[3] += Nq;
+    }
+    T.sync();
+    int n_cand = cand[0];
+    int best_r = ev.m_run, best_a = ev.m_all, best_tau = ev.tau, best_trun = ev.t_run;
+    for (int c = 0; c < n_cand; ++c) {
+      int b, pAr, pNr, pAq, pNq;
+      if (n_cand <= 16) {
+        const int* cd = cand + 1 + 5 * c;
+        b = cd[0];
+        pAr = cd[1];
+        pNr = cd[2];
+        pAq = cd[3];
+        pNq = cd[4];
       } else {
-        hi = mid;
+        // more than 16 candidates (pathological): treat every bin as a candidate,
+        // recomputing the prefix before bin c by a team reduction.
+        b = c;
+        if (b >= NB) break;
+        int v4[4] = {0, 0, 0, 0};
+        for (int y = tid; y < b; y += TT) {
+          int A, N, Aq, Nq;
+          bin_an(binR, y, A, N);
+          bin_an(binQ, y, Aq, Nq);
+          v4[0] += A;
+          v4[1] += N;
+          v4[2] += Aq;
+          v4[3] += Nq;
+        }
+        int t4[4];
+        T.template excl<4>(v4, t4);
+        pAr = t4[0];
+        pNr = t4[1];
+        pAq = t4[2];
+        pNq = t4[3];
+        if (c + 1 == n_cand) n_cand = NB;  // continue over every bin
+      }
+      // gather the bin's included members (r, a, running?)
+      if (tid == 0) memb[0] = 0;
+      T.sync();
+      for (int e = tid; e < n_ent; e += TT) {
+        const uint32_t x = rb[e];
+        if ((int)(x >> 16) == b && (e < k || e - k + 1 <= qlim)) {
+          const int slot = atomicAdd(&memb[0], 1);
+          if (slot < 40) {
+            memb[1 + 3 * slot] = (int)(x & 0xFFFF);
+            memb[2 + 3 * slot] = av[e];
+            memb[3 + 3 * slot] = e < k;
+          }
+        }
+      }
+      T.sync();
+      const int nm = memb[0];
+      int vr = 0, va = 0, tau = 0, trun = 0;
+      if (nm <= 40) {
+        for (int x = tid; x < nm; x += TT) {
+          const int rx = memb[1 + 3 * x];
+          int Ar = pAr, Nr = pNr, Aa = pAr + pAq, Na = pNr + pNq;
+          for (int y = 0; y < nm; ++y) {
+            const int ry = memb[1 + 3 * y], ay = memb[2 + 3 * y], run = memb[3 + 3 * y];
+            const bool ge = ry >= rx;
+            Aa += ge ? ay : 0;
+            Na += ge ? 1 : 0;
+            Ar += (ge && run) ? ay : 0;
+            Nr += (ge && run) ? 1 : 0;
+          }
+          const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;  // exact T at τ = rx
+          vr = ::max(vr, t_r);
+          if (t_a > va) {
+            va = t_a;
+            tau = rx;
+            trun = t_r;
+          }
+        }
+      } else {
+        // many members in one bin (pathological): every member is visited by the
+        // thread owning it, comparing against all requests of the bin.
+        for (int ex = tid; ex < n_ent; ex += TT) {
+          const uint32_t z = rb[ex];
+          if ((int)(z >> 16) != b || !(ex < k || ex - k + 1 <= qlim)) continue;
+          const int rx = (int)(z & 0xFFFF);
+          int Ar = pAr, Nr = pNr, Aa = pAr + pAq, Na = pNr + pNq;
+          for (int e = 0; e < n_ent; ++e) {
+            const uint32_t y = rb[e];
+            if ((int)(y >> 16) != b || !(e < k || e - k + 1 <= qlim)) continue;
+            const bool ge = (int)(y & 0xFFFF) >= rx;
+            Aa += ge ? av[e] : 0;
+            Na += ge ? 1 : 0;
+            Ar += (ge && e < k) ? av[e] : 0;
+            Nr += (ge && e < k) ? 1 : 0;
+          }
+          const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;
+          vr = ::max(vr, t_r);
+          if (t_a > va) {
+            va = t_a;
+            tau = rx;
+            trun = t_r;
+          }
+        }
+      }
+      best_r = ::max(best_r, T.max(vr));
+      const int ma = T.max(va);
+      if (ma > best_a) {
+        best_a = ma;
+        T.pick(va == ma, tau, trun);
+        best_tau = tau;
+        best_trun = trun;
+      }
+      T.sync();
+    }
+    ev.m_run = best_r;
+    ev.m_all = best_a;
+    ev.tau = best_tau;
+    ev.t_run = best_trun;
+    return ev;
+  };
+
+  // ---- a7: Alg.1 lines 7-14 — exact p* by cutting planes (header comment). The
+  // first pass evaluates M*(R) and M*(R ∪ Q); later passes M*(p̂). One call site.
+  int p_star = 0, peak = 0, M0 = 0, ph = q;
+  bool first = true;
+  for (;;) {
+    const Eval ev = evaluate(ph);
+    if (first) {
+      first = false;
+      M0 = ev.m_run;  // Eq.(eq:3): M*(R)
+      if (estimate_only) {
+        if (tid == 0) p.peak_out[i] = M0;
+        return;
+      }
+      if (q == 0 || M0 > Cmax) {
+        p_star = 0;
+        peak = M0;
+        break;
+      }
+      if (ev.m_all <= Cmax) {
+        p_star = q;
+        peak = ev.m_all;
+        break;
+      }
+    } else if (ev.m_all <= Cmax) {
+      p_star = ph;
+      peak = ev.m_all;
+      break;
+    }
+    // p_max(τ*): FIFO prefix of (a_j + τ*)·[r_j ≥ τ*]; first j with T_R(τ*) + prefix > C
+    const int tau = ev.tau;
+    int first_bad = 0x7FFFFFFF, carry = ev.t_run;
+#pragma unroll 1
+    for (int j0 = 0; j0 < ph; j0 += TT) {
+      const int jx = j0 + tid;  // queue index j-1
+      int wv = 0;
+      if (jx < ph) {
+        const int r = (int)(rb[k + jx] & 0xFFFF);
+        wv = (r >= tau) ? av[k + jx] + tau : 0;
+      }
+      int v[1] = {wv}, tot[1];
+      T.template excl<1>(v, tot);
+      if (jx < ph && carry + v[0] + wv > Cmax) first_bad = ::min(first_bad, jx + 1);
+      carry += tot[0];
+      if (T.any(first_bad != 0x7FFFFFFF)) break;
+    }
+    ph = -T.max(-first_bad) - 1;  // p_max(τ*) < previous p̂ (τ* violated there)
+    // rebuild binQ with queue positions 1..ph for the next evaluation
+    {
+      uint4* z4 = reinterpret_cast<uint4*>(binQ);
+#pragma unroll
+      for (int x = 0; x < NBW / 4 / TT; ++x) z4[tid + x * TT] = make_uint4(0, 0, 0, 0);
+    }
+    T.sync();
+    for (int jx = tid; jx < ph; jx += TT) {
+      const uint32_t x = rb[k + jx];
+      const int b = (int)(x >> 16), a = av[k + jx];
+      if (PACK) {
+        atomicAdd(&binQ[b], ((uint32_t)a << 9) | 1u);
+      } else {
+        atomicAdd(&binQ[b], (uint32_t)a);
+        atomicAdd(&binQ[NB + b], 1u);
       }
     }
-    p_star = lo;
-    peak = m_lo;
+    T.sync();
   }
   if (tid == 0) {
     p.admitted_out[i] = p_star;

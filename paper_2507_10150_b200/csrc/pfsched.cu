@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/pfsched.h"
 #include "pf_admit.cuh"
@@ -36,21 +37,34 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 enum Layout { LAYOUT_SORTED = 0, LAYOUT_HIST = 1, LAYOUT_GROUP = 2 };
 
-// Admit-kernel variants: (threads per instance, items per thread).
+// Admit-kernel variants: warps per instance team x lookup x packing.
 typedef void (*AdmitFn)(pf::AdmitParams);
 struct Variant {
-  int T, IPT;
-  AdmitFn fn[3];
+  int TW, cap;       // team warps, max requests per instance served
+  AdmitFn fn[3][2];  // [lookup][pack]
 };
-
-#define PF_VARIANT(T, IPT)                                                                   \
-  {T, IPT, {pf::admit_kernel<T, IPT, pf::LOOK_SORTED>, pf::admit_kernel<T, IPT, pf::LOOK_HIST>, \
-            pf::admit_kernel<T, IPT, pf::LOOK_GROUP>}}
-const Variant kVariants[] = {
-    PF_VARIANT(128, 1), PF_VARIANT(128, 2), PF_VARIANT(128, 4), PF_VARIANT(256, 3),
-    PF_VARIANT(256, 4), PF_VARIANT(256, 5), PF_VARIANT(256, 8), PF_VARIANT(256, 16),
-};
+#define PF_VARIANT(TW, CAP)                                                                      \
+  {TW, CAP,                                                                                     \
+   {{pf::admit_kernel<TW, pf::LOOK_SORTED, false>, pf::admit_kernel<TW, pf::LOOK_SORTED, true>}, \
+    {pf::admit_kernel<TW, pf::LOOK_HIST, false>, pf::admit_kernel<TW, pf::LOOK_HIST, true>},     \
+    {pf::admit_kernel<TW, pf::LOOK_GROUP, false>, pf::admit_kernel<TW, pf::LOOK_GROUP, true>}}}
+const Variant kVariants[] = {PF_VARIANT(1, 512), PF_VARIANT(2, 1024), PF_VARIANT(4, 2048),
+                             PF_VARIANT(8, 4096)};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+inline int teams_per_cta(int TW) { return TW == 1 ? 4 : 1; }
+
+// Host copy of the kernel's log-linear bin map f(r) (pf_admit.cuh header): width-1
+// bins for r ≤ 16, 8 bins per octave up to width 2^s, then width 2^s.
+int bin_f(int r, int s) {
+  if (r <= 16) return r - 1;
+  const int r0 = 1 << (s + 3);
+  if (r < r0) {
+    int o = 0;
+    while ((2 << o) <= r) ++o;
+    return 16 + 8 * (o - 4) + ((r - (1 << o)) >> (o - 3));
+  }
+  return 16 + 8 * (s - 1) + ((r - r0) >> s);
+}
 
 }  // namespace
 
@@ -69,8 +83,12 @@ struct pf_ctx {
   int32_t* group_off = nullptr;
   int* err = nullptr;  // [2] code, index
   int* scratch = nullptr;
+  uint16_t* bintab = nullptr;  // [Lmax+1] r -> bin
+  uint32_t* edges = nullptr;   // [n_bins] lo | hi << 16
+  int pack;
   int variant;
-  size_t admit_smem;
+  size_t admit_smem;   // per CTA
+  int team_smem, ent_cap;
   int n_bins, bin_shift;
 };
 
@@ -80,7 +98,8 @@ void free_ctx(pf_ctx* c) {
   if (!c) return;
   for (void* p : {(void*)c->ring, (void*)c->head, (void*)c->sorted, (void*)c->hist,
                   (void*)c->xbuf, (void*)c->gC, (void*)c->gS, (void*)c->dist_of,
-                  (void*)c->group_off, (void*)c->err, (void*)c->scratch})
+                  (void*)c->group_off, (void*)c->err, (void*)c->scratch, (void*)c->bintab,
+                  (void*)c->edges})
     if (p) cudaFree(p);
   delete c;
 }
@@ -222,21 +241,43 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   // Admit-kernel variant and its shared memory footprint.
   c->variant = -1;
   for (int v = 0; v < kNumVariants; ++v)
-    if (kVariants[v].T * kVariants[v].IPT >= C.max_entries) { c->variant = v; break; }
+    if (kVariants[v].cap >= C.max_entries) { c->variant = v; break; }
   const Variant& V = kVariants[c->variant];
-  c->n_bins = 2 * V.T;
-  c->bin_shift = 0;
-  while (((C.max_len - 1) >> c->bin_shift) >= c->n_bins) ++c->bin_shift;
+  c->n_bins = 128 * V.TW;
+  c->bin_shift = 1;
+  while (bin_f(C.max_len, c->bin_shift) > c->n_bins - 1) ++c->bin_shift;
+  {  // r -> bin table and per-bin r ranges
+    std::vector<uint16_t> tab(C.max_len + 1, 0);
+    std::vector<uint32_t> ed(c->n_bins, 0);
+    for (int r = 1; r <= C.max_len; ++r) {
+      const int b = c->n_bins - 1 - bin_f(r, c->bin_shift);
+      tab[r] = (uint16_t)b;
+      const uint32_t lo = ed[b] ? (ed[b] & 0xFFFF) : (uint32_t)r;
+      ed[b] = lo | ((uint32_t)r << 16);
+    }
+    PF_CUDA_C(cudaMalloc(&c->bintab, tab.size() * 2 + 16));
+    PF_CUDA_C(cudaMalloc(&c->edges, ed.size() * 4 + 16));
+    PF_CUDA_C(cudaMemcpy(c->bintab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice));
+    PF_CUDA_C(cudaMemcpy(c->edges, ed.data(), ed.size() * 4, cudaMemcpyHostToDevice));
+  }
+  // per-bin (A, N) fit one 32-bit word (A << 9 | N) when every bin sum < 2^23 and count < 2^9
+  c->pack = (C.max_entries < 512 &&
+             (int64_t)C.max_entries * ((int64_t)C.max_input_len + C.max_len) < (1LL << 23)) ? 1 : 0;
   size_t table = 0;
   if (c->layout == LAYOUT_SORTED) table = (size_t)C.window * 4;
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
-  c->admit_smem = (size_t)16 * V.T * V.IPT + (size_t)8 * c->n_bins + 64 * 4 + table;
+  c->ent_cap = (C.max_entries + 7) & ~7;
+  const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
+  size_t team = (size_t)c->ent_cap * 8 + nbw * 8 + 256 * 4 + table;
+  team = (team + 15) & ~(size_t)15;
+  c->team_smem = (int)team;
+  c->admit_smem = (size_t)c->n_bins * 4 + team * teams_per_cta(V.TW);
   const int look = c->layout;
   if (c->admit_smem > 227 * 1024) {
     fail(PF_ERANGE, "admit kernel needs %zu B of shared memory", c->admit_smem);
     return cleanup_fail(PF_ERANGE);
   }
-  PF_CUDA_C(cudaFuncSetAttribute(V.fn[look], cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PF_CUDA_C(cudaFuncSetAttribute(V.fn[look][c->pack], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->admit_smem));
 #undef PF_CUDA_C
   *out = c;
@@ -312,8 +353,10 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.instance_base = C.instance_base;
   p.members_per_group = C.members_per_group;
   p.member_base = C.member_base;
-  p.bin_shift = c->bin_shift;
-  p.n_bins = c->n_bins;
+  p.bintab = c->bintab;
+  p.edges = c->edges;
+  p.team_smem = c->team_smem;
+  p.ent_cap = c->ent_cap;
   p.sorted = c->sorted;
   p.hist = c->hist;
   p.gC = c->gC;
@@ -334,7 +377,9 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.pred_q_out = pred_q_out;
   p.err = c->err;
   const Variant& V = kVariants[c->variant];
-  V.fn[c->layout]<<<C.n_instances, V.T, c->admit_smem, s>>>(p);
+  const int teams = teams_per_cta(V.TW);
+  const int grid = (C.n_instances + teams - 1) / teams;
+  V.fn[c->layout][c->pack]<<<grid, teams * V.TW * 32, c->admit_smem, s>>>(p);
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
