@@ -53,8 +53,9 @@ struct AdmitParams {
   // history tables
   const int32_t* sorted;     // LOOK_SORTED [n × w]
   const int32_t* hist;       // LOOK_HIST   [n × (Lmax+1)]
-  const int32_t* gC;         // LOOK_GROUP  [G × (Lmax+1)]
-  const int32_t* gS;         // LOOK_GROUP  [G × W]
+  const uint16_t* gC;        // LOOK_GROUP  [G × c_stride]: C_g[l] = #{h ≤ l} (u16, W < 2^16)
+  const uint16_t* gS;        // LOOK_GROUP  [G × s_stride]: sorted group window (u16)
+  int c_stride, s_stride;    // row strides (multiples of 8 elements)
   const int32_t* dist_of;    // LOOK_GROUP  [n]
   const int32_t* group_off;  // LOOK_GROUP  [G+1]
   // inputs
@@ -253,13 +254,13 @@ admit_kernel(AdmitParams p) {
 
   // ---- a3: the distribution P(l) of Eq.(eq:5) as a lookup structure
   const int w = p.w;
-  const int32_t* gC = nullptr;
-  const int32_t* gS = nullptr;
+  const uint16_t* gC = nullptr;
+  const uint16_t* gS = nullptr;
   int64_t gid;
   if (LOOK == LOOK_GROUP) {
     const int g = p.dist_of[i];
-    gC = p.gC + (int64_t)g * (p.max_len + 1);
-    gS = p.gS + (int64_t)g * w;
+    gC = p.gC + (int64_t)g * p.c_stride;
+    gS = p.gS + (int64_t)g * p.s_stride;
     gid = (int64_t)g * p.members_per_group + p.member_base + (i - p.group_off[g]);
   } else {
     gid = p.instance_base + i;
@@ -329,7 +330,7 @@ admit_kernel(AdmitParams p) {
       const int n_gt = w - bq[c];
       const int x = bq[c] + (int)__umulhi(u[c], (uint32_t)n_gt);
       if (LOOK == LOOK_GROUP) {
-        lh[c] = n_gt ? __ldg(gS + x) : max_new;
+        lh[c] = n_gt ? (int)__ldg(gS + x) : max_new;
       } else if (LOOK == LOOK_SORTED) {
         lh[c] = n_gt ? table[x] : max_new;
       } else {

@@ -192,16 +192,18 @@ __global__ void update_hist_kernel(int n_rows, int row_window, int rows_per_hist
 }
 
 // Group tables from the (all-reduced) group histogram H_g: C_g[l] = Σ_{l'≤l} H_g[l']
-// and the sorted window S_g (S_g[x] = l for x ∈ [C_g[l−1], C_g[l])). CTA per group.
+// and the sorted window S_g (S_g[x] = l for x ∈ [C_g[l−1], C_g[l])), both u16 (W < 2^16,
+// Lmax < 2^15) with row strides c_stride / s_stride. CTA per group.
 template <int T>
 __global__ void __launch_bounds__(T) group_tables_kernel(const int32_t* H, int max_len, int W,
-                                                         int32_t* gC, int32_t* gS) {
+                                                         int c_stride, int s_stride, uint16_t* gC,
+                                                         uint16_t* gS) {
   __shared__ int scratch[64];
   const int g = blockIdx.x;
   const int nb = max_len + 1;
   const int32_t* h = H + (int64_t)g * nb;
-  int32_t* C = gC + (int64_t)g * nb;
-  int32_t* S = gS + (int64_t)g * W;
+  uint16_t* C = gC + (int64_t)g * c_stride;
+  uint16_t* S = gS + (int64_t)g * s_stride;
   const int per = (nb + T - 1) / T;
   const int lo = threadIdx.x * per, hi = min(nb, lo + per);
   int s = 0;
@@ -212,8 +214,8 @@ __global__ void __launch_bounds__(T) group_tables_kernel(const int32_t* H, int m
   for (int l = lo; l < hi; ++l) {
     const int prev = acc;
     acc += h[l];
-    C[l] = acc;
-    for (int x = prev; x < acc && x < W; ++x) S[x] = l;
+    C[l] = (uint16_t)min(acc, 65535);
+    for (int x = prev; x < acc && x < W; ++x) S[x] = (uint16_t)l;
   }
 }
 

@@ -77,8 +77,9 @@ struct pf_ctx {
   int32_t* sorted = nullptr;  // LAYOUT_SORTED
   int32_t* hist = nullptr;    // LAYOUT_HIST: per instance; LAYOUT_GROUP: partial (owned shards)
   int32_t* xbuf = nullptr;    // LAYOUT_GROUP exchange buffer [G × (Lmax+1)]
-  int32_t* gC = nullptr;
-  int32_t* gS = nullptr;
+  uint16_t* gC = nullptr;  // [G × c_stride] u16
+  uint16_t* gS = nullptr;  // [G × s_stride] u16
+  int c_stride = 0, s_stride = 0;
   int32_t* dist_of = nullptr;
   int32_t* group_off = nullptr;
   int* err = nullptr;  // [2] code, index
@@ -120,8 +121,8 @@ int grid_for(int64_t total, int threads) {
 }
 
 pf_status build_group_tables(pf_ctx* c, cudaStream_t s) {
-  pf::group_tables_kernel<256><<<c->cfg.n_groups, 256, 0, s>>>(c->xbuf, c->cfg.max_len,
-                                                               c->cfg.window, c->gC, c->gS);
+  pf::group_tables_kernel<256><<<c->cfg.n_groups, 256, 0, s>>>(
+      c->xbuf, c->cfg.max_len, c->cfg.window, c->c_stride, c->s_stride, c->gC, c->gS);
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
@@ -154,6 +155,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   if (C.n_groups > 0) {
     if (C.window % 8) return fail(PF_EINVAL, "shared mode: window must be a multiple of 8");
     if (!C.group_off) return fail(PF_EINVAL, "shared mode: group_off required");
+    if (C.window > 65535) return fail(PF_ERANGE, "shared mode: window must be < 65536");
     if (C.nranks < 1 || 8 % C.nranks || C.rank < 0 || C.rank >= C.nranks)
       return fail(PF_EINVAL, "shared mode: nranks must divide 8 and 0 <= rank < nranks");
   } else if (C.window > 16384 && C.window <= C.max_len + 1) {
@@ -217,8 +219,12 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   if (c->layout == LAYOUT_GROUP) {
     const int G = C.n_groups;
     PF_CUDA_C(cudaMalloc(&c->xbuf, (size_t)G * nb * 4 + 16));
-    PF_CUDA_C(cudaMalloc(&c->gC, (size_t)G * nb * 4 + 16));
-    PF_CUDA_C(cudaMalloc(&c->gS, (size_t)G * C.window * 4 + 16));
+    c->c_stride = (nb + 7) & ~7;
+    c->s_stride = (C.window + 7) & ~7;
+    PF_CUDA_C(cudaMalloc(&c->gC, (size_t)G * c->c_stride * 2 + 16));
+    PF_CUDA_C(cudaMalloc(&c->gS, (size_t)G * c->s_stride * 2 + 16));
+    PF_CUDA_C(cudaMemsetAsync(c->gC, 0, (size_t)G * c->c_stride * 2, s));
+    PF_CUDA_C(cudaMemsetAsync(c->gS, 0, (size_t)G * c->s_stride * 2, s));
     PF_CUDA_C(cudaMalloc(&c->dist_of, (size_t)C.n_instances * 4 + 16));
     PF_CUDA_C(cudaMalloc(&c->group_off, (size_t)(G + 1) * 4 + 16));
     PF_CUDA_C(cudaMemcpyAsync(c->group_off, C.group_off, (size_t)(G + 1) * 4,
@@ -361,6 +367,8 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.hist = c->hist;
   p.gC = c->gC;
   p.gS = c->gS;
+  p.c_stride = c->c_stride;
+  p.s_stride = c->s_stride;
   p.dist_of = c->dist_of;
   p.group_off = c->group_off;
   p.run_off = run_off;
