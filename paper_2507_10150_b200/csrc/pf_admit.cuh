@@ -162,13 +162,13 @@ struct Team {
       v2 = __shfl_sync(0xffffffffu, v2, who);
     } else {
       const int who = -this->max(own ? -tid : -(1 << 20));
-      if (tid == who) {  // xs[120..121]: between the candidate and member lists
-        xs[120] = v1;
-        xs[121] = v2;
+      if (tid == who) {  // xs[32..33]
+        xs[32] = v1;
+        xs[33] = v2;
       }
       sync();
-      v1 = xs[120];
-      v2 = xs[121];
+      v1 = xs[32];
+      v2 = xs[33];
       sync();
     }
   }
@@ -183,11 +183,13 @@ struct Eval {
 };
 
 // Per-team shared memory layout (bytes, in order):
-//   rb[ent_cap] u32  (r | bin << 16, original request order: e < k running, then queue)
-//   av[ent_cap] u32  (a = l_p + l_t)
+//   rb[ent_cap] u32  request records in original order (e < k running, then queue):
+//                    PACK: r | a << 13 (r < 2^13, a < 2^19); else r | bin << 16 and
+//   av[ent_cap] u32  a = l_p + l_t (absent when PACK)
+//   ml[ent_cap] u16  member list of the exact refinement (e | candidate << 12)
 //   binR[NBW] u32, binQ[NBW] u32: per-bin (A, N) — packed A << 9 | N when PACK, else
 //                    A in [0, NB) and N in [NB, 2·NB)
-//   xs[256] i32      scratch: reductions, candidate list, member list
+//   xs[160] i32      scratch: reductions [0,32), pick [32,34), list size [36], candidates [40,137)
 //   table            S[w] (LOOK_SORTED) | C[Lmax+1] (LOOK_HIST)
 // CTA prefix: edges[NB] u32 shared by the teams.
 template <int TW, int LOOK, bool PACK>
@@ -210,13 +212,15 @@ admit_kernel(AdmitParams p) {
   T.wid = T.tid >> 5;
   unsigned char* base = smem_raw + NB * 4 + (size_t)T.id * p.team_smem;
   uint32_t* rb = reinterpret_cast<uint32_t*>(base);
-  int* av = reinterpret_cast<int*>(rb + p.ent_cap);
-  uint32_t* binR = reinterpret_cast<uint32_t*>(av + p.ent_cap);
+  int* av = reinterpret_cast<int*>(rb + p.ent_cap);  // unused when PACK
+  uint16_t* ml = reinterpret_cast<uint16_t*>(av + (PACK ? 0 : p.ent_cap));
+  uint32_t* binR = reinterpret_cast<uint32_t*>(ml + p.ent_cap);
   uint32_t* binQ = binR + NBW;
   T.xs = reinterpret_cast<int*>(binQ + NBW);
-  int* cand = T.xs + 32;    // [0]: count, then 5 ints per candidate (≤ 16)
-  int* memb = T.xs + 128;   // [0]: count, then (r, a, is_run) per member (≤ 40)
-  int32_t* table = T.xs + 256;
+  int* cand = T.xs + 40;    // [0]: count, then 6 ints per candidate (≤ 16); xs[36]: list size
+  auto ent_r = [&](int e) -> int { return (int)(rb[e] & (PACK ? 0x1FFFu : 0xFFFFu)); };
+  auto ent_a = [&](int e) -> int { return PACK ? (int)(rb[e] >> 13) : av[e]; };
+  int32_t* table = T.xs + 160;
 
   const int i = blockIdx.x * TEAMS + T.id;
   if (i >= p.n) return;
@@ -357,8 +361,12 @@ admit_kernel(AdmitParams p) {
         const int r = l_hat - lt[c];  // ≥ 1 (C-4)
         const int a = lp[c] + lt[c];
         const int b = __ldg(p.bintab + r);
-        rb[e] = (uint32_t)r | ((uint32_t)b << 16);
-        av[e] = a;
+        if (PACK) {
+          rb[e] = (uint32_t)r | ((uint32_t)a << 13);
+        } else {
+          rb[e] = (uint32_t)r | ((uint32_t)b << 16);
+          av[e] = a;
+        }
         uint32_t* bins = run ? binR : binQ;
         if (PACK) {
           atomicAdd(&bins[b], ((uint32_t)a << 9) | 1u);
@@ -475,7 +483,8 @@ admit_kernel(AdmitParams p) {
       if (c_r || c_a) {
         const int slot = atomicAdd(&cand[0], 1);
         if (slot < 16) {
-          int* cd = cand + 1 + 5 * slot;
+          int* cd = cand + 1 + 6 * slot;
+          cd[5] = (int)ed;  // lo | hi << 16
           cd[0] = b0 + x;
           cd[1] = s[0];  // A_R, N_R, A_Q', N_Q' over the bins before b
           cd[2] = s[1];
@@ -489,113 +498,80 @@ admit_kernel(AdmitParams p) {
       s[3] += Nq;
     }
     T.sync();
-    int n_cand = cand[0];
+    const int n_cand = cand[0];
     int best_r = ev.m_run, best_a = ev.m_all, best_tau = ev.tau, best_trun = ev.t_run;
-    for (int c = 0; c < n_cand; ++c) {
-      int b, pAr, pNr, pAq, pNq;
-      if (n_cand <= 16) {
-        const int* cd = cand + 1 + 5 * c;
-        b = cd[0];
-        pAr = cd[1];
-        pNr = cd[2];
-        pAq = cd[3];
-        pNq = cd[4];
-      } else {
-        // more than 16 candidates (pathological): treat every bin as a candidate,
-        // recomputing the prefix before bin c by a team reduction.
-        b = c;
-        if (b >= NB) break;
-        int v4[4] = {0, 0, 0, 0};
-        for (int y = tid; y < b; y += TT) {
-          int A, N, Aq, Nq;
-          bin_an(binR, y, A, N);
-          bin_an(binQ, y, Aq, Nq);
-          v4[0] += A;
-          v4[1] += N;
-          v4[2] += Aq;
-          v4[3] += Nq;
-        }
-        int t4[4];
-        T.template excl<4>(v4, t4);
-        pAr = t4[0];
-        pNr = t4[1];
-        pAq = t4[2];
-        pNq = t4[3];
-        if (c + 1 == n_cand) n_cand = NB;  // continue over every bin
-      }
-      // gather the bin's included members (r, a, running?)
-      if (tid == 0) memb[0] = 0;
+    int vr = 0, va = 0, tau = 0, trun = 0;
+    if (n_cand <= 16) {
+      // one pass: list the included requests whose r lies in a candidate bin's range
+      if (tid == 0) T.xs[36] = 0;
       T.sync();
       for (int e = tid; e < n_ent; e += TT) {
-        const uint32_t x = rb[e];
-        if ((int)(x >> 16) == b && (e < k || e - k + 1 <= qlim)) {
-          const int slot = atomicAdd(&memb[0], 1);
-          if (slot < 40) {
-            memb[1 + 3 * slot] = (int)(x & 0xFFFF);
-            memb[2 + 3 * slot] = av[e];
-            memb[3 + 3 * slot] = e < k;
-          }
+        if (e >= k && e - k + 1 > qlim) continue;  // queue request not in Q'
+        const int r = ent_r(e);
+        for (int c = 0; c < n_cand; ++c) {
+          const uint32_t ed = (uint32_t)cand[1 + 6 * c + 5];
+          if (r >= (int)(ed & 0xFFFF) && r <= (int)(ed >> 16))
+            ml[atomicAdd(&T.xs[36], 1)] = (uint16_t)(e | (c << 12));
         }
       }
       T.sync();
-      const int nm = memb[0];
-      int vr = 0, va = 0, tau = 0, trun = 0;
-      if (nm <= 40) {
-        for (int x = tid; x < nm; x += TT) {
-          const int rx = memb[1 + 3 * x];
-          int Ar = pAr, Nr = pNr, Aa = pAr + pAq, Na = pNr + pNq;
-          for (int y = 0; y < nm; ++y) {
-            const int ry = memb[1 + 3 * y], ay = memb[2 + 3 * y], run = memb[3 + 3 * y];
-            const bool ge = ry >= rx;
-            Aa += ge ? ay : 0;
-            Na += ge ? 1 : 0;
-            Ar += (ge && run) ? ay : 0;
-            Nr += (ge && run) ? 1 : 0;
-          }
-          const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;  // exact T at τ = rx
-          vr = ::max(vr, t_r);
-          if (t_a > va) {
-            va = t_a;
-            tau = rx;
-            trun = t_r;
-          }
+      const int nm = T.xs[36];
+      // exact T at every member's r: prefix before its bin + the bin's members with r ≥
+      for (int x = tid; x < nm; x += TT) {
+        const int mx = ml[x], ex = mx & 0xFFF, cx = mx >> 12;
+        const int rx = ent_r(ex);
+        const int* cd = cand + 1 + 6 * cx;
+        int Ar = cd[1], Nr = cd[2], Aa = cd[1] + cd[3], Na = cd[2] + cd[4];
+        for (int y = 0; y < nm; ++y) {
+          const int my = ml[y], ey = my & 0xFFF;
+          const bool ge = (my >> 12) == cx && ent_r(ey) >= rx;
+          const int ay = ge ? ent_a(ey) : 0;
+          Aa += ay;
+          Na += ge ? 1 : 0;
+          Ar += (ey < k) ? ay : 0;
+          Nr += (ge && ey < k) ? 1 : 0;
         }
-      } else {
-        // many members in one bin (pathological): every member is visited by the
-        // thread owning it, comparing against all requests of the bin.
-        for (int ex = tid; ex < n_ent; ex += TT) {
-          const uint32_t z = rb[ex];
-          if ((int)(z >> 16) != b || !(ex < k || ex - k + 1 <= qlim)) continue;
-          const int rx = (int)(z & 0xFFFF);
-          int Ar = pAr, Nr = pNr, Aa = pAr + pAq, Na = pNr + pNq;
-          for (int e = 0; e < n_ent; ++e) {
-            const uint32_t y = rb[e];
-            if ((int)(y >> 16) != b || !(e < k || e - k + 1 <= qlim)) continue;
-            const bool ge = (int)(y & 0xFFFF) >= rx;
-            Aa += ge ? av[e] : 0;
-            Na += ge ? 1 : 0;
-            Ar += (ge && e < k) ? av[e] : 0;
-            Nr += (ge && e < k) ? 1 : 0;
-          }
-          const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;
-          vr = ::max(vr, t_r);
-          if (t_a > va) {
-            va = t_a;
-            tau = rx;
-            trun = t_r;
-          }
+        const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;  // exact T at τ = rx
+        vr = ::max(vr, t_r);
+        if (t_a > va) {
+          va = t_a;
+          tau = rx;
+          trun = t_r;
         }
       }
-      best_r = ::max(best_r, T.max(vr));
-      const int ma = T.max(va);
-      if (ma > best_a) {
-        best_a = ma;
-        T.pick(va == ma, tau, trun);
-        best_tau = tau;
-        best_trun = trun;
+    } else {
+      // Pathological spread (> 16 candidate bins): exact T at every included request.
+      for (int ex = tid; ex < n_ent; ex += TT) {
+        if (ex >= k && ex - k + 1 > qlim) continue;
+        const int rx = ent_r(ex);
+        int Ar = 0, Nr = 0, Aa = 0, Na = 0;
+        for (int e = 0; e < n_ent; ++e) {
+          if (e >= k && e - k + 1 > qlim) continue;
+          const bool ge = ent_r(e) >= rx;
+          const int ae = ge ? ent_a(e) : 0;
+          Aa += ae;
+          Na += ge ? 1 : 0;
+          Ar += (e < k) ? ae : 0;
+          Nr += (ge && e < k) ? 1 : 0;
+        }
+        const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;
+        vr = ::max(vr, t_r);
+        if (t_a > va) {
+          va = t_a;
+          tau = rx;
+          trun = t_r;
+        }
       }
-      T.sync();
     }
+    best_r = ::max(best_r, T.max(vr));
+    const int ma = T.max(va);
+    if (ma > best_a) {
+      best_a = ma;
+      T.pick(va == ma, tau, trun);
+      best_tau = tau;
+      best_trun = trun;
+    }
+    T.sync();
     ev.m_run = best_r;
     ev.m_all = best_a;
     ev.tau = best_tau;
@@ -639,8 +615,8 @@ admit_kernel(AdmitParams p) {
       const int jx = j0 + tid;  // queue index j-1
       int wv = 0;
       if (jx < ph) {
-        const int r = (int)(rb[k + jx] & 0xFFFF);
-        wv = (r >= tau) ? av[k + jx] + tau : 0;
+        const int r = ent_r(k + jx);
+        wv = (r >= tau) ? ent_a(k + jx) + tau : 0;
       }
       int v[1] = {wv}, tot[1];
       T.template excl<1>(v, tot);
@@ -657,8 +633,8 @@ admit_kernel(AdmitParams p) {
     }
     T.sync();
     for (int jx = tid; jx < ph; jx += TT) {
-      const uint32_t x = rb[k + jx];
-      const int b = (int)(x >> 16), a = av[k + jx];
+      const int b = PACK ? (int)__ldg(p.bintab + ent_r(k + jx)) : (int)(rb[k + jx] >> 16);
+      const int a = ent_a(k + jx);
       if (PACK) {
         atomicAdd(&binQ[b], ((uint32_t)a << 9) | 1u);
       } else {

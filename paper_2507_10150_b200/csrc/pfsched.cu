@@ -266,15 +266,17 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     PF_CUDA_C(cudaMemcpy(c->bintab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice));
     PF_CUDA_C(cudaMemcpy(c->edges, ed.data(), ed.size() * 4, cudaMemcpyHostToDevice));
   }
-  // per-bin (A, N) fit one 32-bit word (A << 9 | N) when every bin sum < 2^23 and count < 2^9
+  // PACK: per-bin (A, N) fit one 32-bit word (A << 9 | N: every bin sum < 2^23, count
+  // < 2^9) and a request record fits one (r | a << 13: Lmax < 2^13, a < 2^19)
   c->pack = (C.max_entries < 512 &&
-             (int64_t)C.max_entries * ((int64_t)C.max_input_len + C.max_len) < (1LL << 23)) ? 1 : 0;
+             (int64_t)C.max_entries * ((int64_t)C.max_input_len + C.max_len) < (1LL << 23) &&
+             C.max_len < 8192 && (int64_t)C.max_input_len + C.max_len < (1LL << 19)) ? 1 : 0;
   size_t table = 0;
   if (c->layout == LAYOUT_SORTED) table = (size_t)C.window * 4;
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
   c->ent_cap = (C.max_entries + 7) & ~7;
   const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
-  size_t team = (size_t)c->ent_cap * 8 + nbw * 8 + 256 * 4 + table;
+  size_t team = (size_t)c->ent_cap * (c->pack ? 6 : 10) + nbw * 8 + 160 * 4 + table;
   team = (team + 15) & ~(size_t)15;
   c->team_smem = (int)team;
   c->admit_smem = (size_t)c->n_bins * 4 + team * teams_per_cta(V.TW);
