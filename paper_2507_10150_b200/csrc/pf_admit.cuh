@@ -186,7 +186,8 @@ struct Eval {
 //   rb[ent_cap] u32  request records in original order (e < k running, then queue):
 //                    PACK: r | a << 13 (r < 2^13, a < 2^19); else r | bin << 16 and
 //   av[ent_cap] u32  a = l_p + l_t (absent when PACK)
-//   ml[ent_cap] u16  member list of the exact refinement (e | candidate << 12)
+//   nx[ent_cap] u16  per-bin linked lists of requests (next index; 0xFFFF ends a list)
+//   hd[NB] u32       list heads, one per bin (built in a4 with atomicExch)
 //   binR[NBW] u32, binQ[NBW] u32: per-bin (A, N) — packed A << 9 | N when PACK, else
 //                    A in [0, NB) and N in [NB, 2·NB)
 //   xs[160] i32      scratch: reductions [0,32), pick [32,34), list size [36], candidates [40,137)
@@ -213,8 +214,9 @@ admit_kernel(AdmitParams p) {
   unsigned char* base = smem_raw + NB * 4 + (size_t)T.id * p.team_smem;
   uint32_t* rb = reinterpret_cast<uint32_t*>(base);
   int* av = reinterpret_cast<int*>(rb + p.ent_cap);  // unused when PACK
-  uint16_t* ml = reinterpret_cast<uint16_t*>(av + (PACK ? 0 : p.ent_cap));
-  uint32_t* binR = reinterpret_cast<uint32_t*>(ml + p.ent_cap);
+  uint16_t* nx = reinterpret_cast<uint16_t*>(av + (PACK ? 0 : p.ent_cap));
+  uint32_t* hd = reinterpret_cast<uint32_t*>(nx + p.ent_cap);
+  uint32_t* binR = hd + NB;
   uint32_t* binQ = binR + NBW;
   T.xs = reinterpret_cast<int*>(binQ + NBW);
   int* cand = T.xs + 40;    // [0]: count, then 6 ints per candidate (≤ 16); xs[36]: list size
@@ -273,6 +275,9 @@ admit_kernel(AdmitParams p) {
     uint4* z4 = reinterpret_cast<uint4*>(binR);  // binR and binQ are contiguous
 #pragma unroll
     for (int x = 0; x < 2 * NBW / 4 / TT; ++x) z4[tid + x * TT] = make_uint4(0, 0, 0, 0);
+    uint4* h4 = reinterpret_cast<uint4*>(hd);  // empty lists
+#pragma unroll
+    for (int x = 0; x < NB / 4 / TT; ++x) h4[tid + x * TT] = make_uint4(~0u, ~0u, ~0u, ~0u);
   }
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
@@ -367,6 +372,7 @@ admit_kernel(AdmitParams p) {
           rb[e] = (uint32_t)r | ((uint32_t)b << 16);
           av[e] = a;
         }
+        nx[e] = (uint16_t)atomicExch(&hd[b], (uint32_t)e);  // push onto bin b's list
         uint32_t* bins = run ? binR : binQ;
         if (PACK) {
           atomicAdd(&bins[b], ((uint32_t)a << 9) | 1u);
@@ -502,41 +508,35 @@ admit_kernel(AdmitParams p) {
     int best_r = ev.m_run, best_a = ev.m_all, best_tau = ev.tau, best_trun = ev.t_run;
     int vr = 0, va = 0, tau = 0, trun = 0;
     if (n_cand <= 16) {
-      // one pass: list the included requests whose r lies in a candidate bin's range
-      if (tid == 0) T.xs[36] = 0;
-      T.sync();
-      for (int e = tid; e < n_ent; e += TT) {
-        if (e >= k && e - k + 1 > qlim) continue;  // queue request not in Q'
-        const int r = ent_r(e);
-        for (int c = 0; c < n_cand; ++c) {
-          const uint32_t ed = (uint32_t)cand[1 + 6 * c + 5];
-          if (r >= (int)(ed & 0xFFFF) && r <= (int)(ed >> 16))
-            ml[atomicAdd(&T.xs[36], 1)] = (uint16_t)(e | (c << 12));
-        }
-      }
-      T.sync();
-      const int nm = T.xs[36];
-      // exact T at every member's r: prefix before its bin + the bin's members with r ≥
-      for (int x = tid; x < nm; x += TT) {
-        const int mx = ml[x], ex = mx & 0xFFF, cx = mx >> 12;
-        const int rx = ent_r(ex);
-        const int* cd = cand + 1 + 6 * cx;
-        int Ar = cd[1], Nr = cd[2], Aa = cd[1] + cd[3], Na = cd[2] + cd[4];
-        for (int y = 0; y < nm; ++y) {
-          const int my = ml[y], ey = my & 0xFFF;
-          const bool ge = (my >> 12) == cx && ent_r(ey) >= rx;
-          const int ay = ge ? ent_a(ey) : 0;
-          Aa += ay;
-          Na += ge ? 1 : 0;
-          Ar += (ey < k) ? ay : 0;
-          Nr += (ge && ey < k) ? 1 : 0;
-        }
-        const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;  // exact T at τ = rx
-        vr = ::max(vr, t_r);
-        if (t_a > va) {
-          va = t_a;
-          tau = rx;
-          trun = t_r;
+      // walk each candidate bin's request list: thread x takes the x-th included member
+      // and sums over the members with r ≥ its r (a second walk)
+      for (int c = 0; c < n_cand; ++c) {
+        const int* cd = cand + 1 + 6 * c;
+        const int head = (int)(hd[cd[0]] & 0xFFFFu);
+        int cnt = 0;
+        for (int e = head; e != 0xFFFF; e = nx[e]) {
+          if (e >= k && e - k + 1 > qlim) continue;  // queue request not in Q'
+          if ((cnt & (TT - 1)) == tid) {  // this thread's member: exact T at its r
+            const int rx = ent_r(e);
+            int Ar = cd[1], Nr = cd[2], Aa = cd[1] + cd[3], Na = cd[2] + cd[4];
+            for (int y = head; y != 0xFFFF; y = nx[y]) {
+              if (y >= k && y - k + 1 > qlim) continue;
+              const bool ge = ent_r(y) >= rx;
+              const int ay = ge ? ent_a(y) : 0;
+              Aa += ay;
+              Na += ge ? 1 : 0;
+              Ar += (y < k) ? ay : 0;
+              Nr += (ge && y < k) ? 1 : 0;
+            }
+            const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;  // exact T at τ = rx
+            vr = ::max(vr, t_r);
+            if (t_a > va) {
+              va = t_a;
+              tau = rx;
+              trun = t_r;
+            }
+          }
+          ++cnt;
         }
       }
     } else {

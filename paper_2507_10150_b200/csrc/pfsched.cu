@@ -276,7 +276,8 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
   c->ent_cap = (C.max_entries + 7) & ~7;
   const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
-  size_t team = (size_t)c->ent_cap * (c->pack ? 6 : 10) + nbw * 8 + 160 * 4 + table;
+  size_t team = (size_t)c->ent_cap * (c->pack ? 6 : 10) + (size_t)c->n_bins * 4 + nbw * 8 +
+                160 * 4 + table;
   team = (team + 15) & ~(size_t)15;
   c->team_smem = (int)team;
   c->admit_smem = (size_t)c->n_bins * 4 + team * teams_per_cta(V.TW);
