@@ -28,6 +28,12 @@
 #pragma once
 #include "pf_common.cuh"
 
+// Bins per thread of the r-bin map (4: 128 bins per warp, 8 sub-bins per octave;
+// 8: 256 bins per warp, 16 per octave). Host and device must agree (pfsched.cu).
+#ifndef PF_BPT
+#define PF_BPT 4
+#endif
+
 namespace pf {
 
 enum Lookup { LOOK_SORTED = 0, LOOK_HIST = 1, LOOK_GROUP = 2 };
@@ -198,8 +204,8 @@ __global__ void __launch_bounds__((TW == 1 ? 4 : 1) * TW * 32, (TW == 1 ? 8 : 2)
 admit_kernel(AdmitParams p) {
   constexpr int TT = TW * 32;
   constexpr int TEAMS = (TW == 1) ? 4 : 1;
-  constexpr int NB = 128 * TW;  // 4 bins per thread
-  constexpr int BPT = 4;
+  constexpr int BPT = PF_BPT;  // bins per thread
+  constexpr int NB = 32 * BPT * TW;
   constexpr int NBW = PACK ? NB : 2 * NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* edges = reinterpret_cast<uint32_t*>(smem_raw);
@@ -298,38 +304,65 @@ admit_kernel(AdmitParams p) {
   }
   T.sync();
 
-  // ---- a4: predictions (Alg.1 lines 3-9), 4 requests per thread per chunk with the
-  // chunk's loads issued together; each request's (a, 1) is added to its r-bin.
+  // ---- a4: predictions (Alg.1 lines 3-9), running rows then queued rows, 4 requests
+  // per thread per chunk with the chunk's loads issued together; each request's (a, 1)
+  // is added to its r-bin and the request is pushed on the bin's list.
   uint32_t key_fold = 0;
   if (p.mode == 0) {
     const uint64_t K = instance_key(p.seed, p.tick, gid);
     key_fold = (uint32_t)K ^ (uint32_t)(K >> 32);
   }
-  const int m_used = (n_ent + TT - 1) / TT;
   const bool want_pred = (p.pred_run_out != nullptr) || (p.pred_q_out != nullptr);
   int my_bad = 0;
+  auto draw = [&](int e) -> uint32_t {
+    if (p.mode != 0) return p.quantile_u;
+    if (p.R == 1) return lowbias32(key_fold ^ ((uint32_t)e * 0x9E3779B9U));
+    return draw_u(key_fold, e, p.R);
+  };
+  // l̂ → r, a; bin; push; (A, N) into the running or queue bins
+  auto finish = [&](int e, int l_hat, int l_t, int l_p, bool run) {
+    l_hat = ::min(l_hat, max_new);  // C-6
+    if (want_pred) {
+      int32_t* pout = run ? p.pred_run_out : p.pred_q_out;
+      if (pout) pout[run ? r0 + e : q0 - k + e] = l_hat;
+    }
+    const int r = l_hat - l_t;  // ≥ 1 (C-4)
+    const int a = l_p + l_t;
+    const int b = __ldg(p.bintab + r);
+    if (PACK) {
+      rb[e] = (uint32_t)r | ((uint32_t)a << 13);
+    } else {
+      rb[e] = (uint32_t)r | ((uint32_t)b << 16);
+      av[e] = a;
+    }
+    nx[e] = (uint16_t)atomicExch(&hd[b], (uint32_t)e);  // push onto bin b's list
+    uint32_t* bins = run ? binR : binQ;
+    if (PACK) {
+      atomicAdd(&bins[b], ((uint32_t)a << 9) | 1u);
+    } else {
+      atomicAdd(&bins[b], (uint32_t)a);
+      atomicAdd(&bins[NB + b], 1u);
+    }
+  };
+  // running requests e ∈ [0, k): l̂ from P(l > l_t)
 #pragma unroll 1
-  for (int m0 = 0; m0 < m_used; m0 += 4) {
+  for (int e0 = tid; e0 < k; e0 += 4 * TT) {
     int lp[4], lt[4], bq[4], lh[4];
     uint32_t u[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int e = tid + (m0 + c) * TT;
-      const bool run = e < k;
-      const int32_t* src = run ? p.input_len + r0 + e : p.q_input_len + (q0 - k) + e;
-      lp[c] = (e < n_ent) ? __ldg(src) : 0;
-      lt[c] = run ? __ldg(p.generated + r0 + e) : 0;
+      const int e = e0 + c * TT;
+      lp[c] = e < k ? __ldg(p.input_len + r0 + e) : 0;
+      lt[c] = e < k ? __ldg(p.generated + r0 + e) : 0;
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int e = tid + (m0 + c) * TT;
+      const int e = e0 + c * TT;
       // l_p ∉ [0, max_input_len] or l_t ∉ [0, max_new) (unsigned compares catch < 0)
-      my_bad |= (e < n_ent) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
-                               ((unsigned)lt[c] >= (unsigned)max_new));
+      my_bad |= (e < k) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
+                           ((unsigned)lt[c] >= (unsigned)max_new));
       lt[c] = ::min(::max(lt[c], 0), max_new - 1);  // keep lookups in range; outputs dropped if bad
-      if (p.mode != 0) u[c] = p.quantile_u;
-      else if (p.R == 1) u[c] = lowbias32(key_fold ^ ((uint32_t)e * 0x9E3779B9U));
-      else u[c] = draw_u(key_fold, e, p.R);
+      u[c] = draw(e);
       if (LOOK == LOOK_GROUP) bq[c] = __ldg(gC + lt[c]);
       else if (LOOK == LOOK_HIST) bq[c] = table[lt[c]];
       else bq[c] = upper_bound_smem(table, w, lt[c]);
@@ -355,32 +388,44 @@ admit_kernel(AdmitParams p) {
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int e = tid + (m0 + c) * TT;
-      if (e < n_ent) {
-        const int l_hat = ::min(lh[c], max_new);
-        const bool run = e < k;
-        if (want_pred) {
-          int32_t* pout = run ? p.pred_run_out : p.pred_q_out;
-          if (pout) pout[run ? r0 + e : q0 - k + e] = l_hat;
+      const int e = e0 + c * TT;
+      if (e < k) finish(e, lh[c], lt[c], lp[c], true);
+    }
+  }
+  // queued requests j ∈ [0, q), slot e = k + j: l̂ from P(l) — every history value
+  // exceeds l_t = 0 (C-16), so base = 0 and n_gt = w: one lookup
+#pragma unroll 1
+  for (int j0 = tid; j0 < q; j0 += 4 * TT) {
+    int lp[4], lh[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + c * TT;
+      lp[c] = j < q ? __ldg(p.q_input_len + q0 + j) : 0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + c * TT;
+      my_bad |= (j < q) & ((unsigned)lp[c] > (unsigned)p.max_input_len);
+      const int x = (int)__umulhi(draw(k + j), (uint32_t)w);
+      if (LOOK == LOOK_GROUP) {
+        lh[c] = __ldg(gS + x);
+      } else if (LOOK == LOOK_SORTED) {
+        lh[c] = table[x];
+      } else {
+        int lo = 1, len = p.max_len;  // smallest L with C[L] > x
+        while (len > 0) {
+          const int half = len >> 1;
+          const bool right = table[lo + half] <= x;
+          lo = right ? lo + half + 1 : lo;
+          len = right ? len - half - 1 : half;
         }
-        const int r = l_hat - lt[c];  // ≥ 1 (C-4)
-        const int a = lp[c] + lt[c];
-        const int b = __ldg(p.bintab + r);
-        if (PACK) {
-          rb[e] = (uint32_t)r | ((uint32_t)a << 13);
-        } else {
-          rb[e] = (uint32_t)r | ((uint32_t)b << 16);
-          av[e] = a;
-        }
-        nx[e] = (uint16_t)atomicExch(&hd[b], (uint32_t)e);  // push onto bin b's list
-        uint32_t* bins = run ? binR : binQ;
-        if (PACK) {
-          atomicAdd(&bins[b], ((uint32_t)a << 9) | 1u);
-        } else {
-          atomicAdd(&bins[b], (uint32_t)a);
-          atomicAdd(&bins[NB + b], 1u);
-        }
+        lh[c] = lo;
       }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + c * TT;
+      if (j < q) finish(k + j, lh[c], 0, lp[c], false);
     }
   }
   if (T.any(my_bad != 0)) {
@@ -421,16 +466,49 @@ admit_kernel(AdmitParams p) {
   };
   auto evaluate = [&](int qlim) -> Eval {
     const int b0 = tid * BPT;
+    // this thread's bins in registers (16-byte shared loads)
+    int bA[BPT], bN[BPT], qA[BPT], qN[BPT];
+    uint32_t ed[BPT];
+#pragma unroll
+    for (int x0 = 0; x0 < BPT; x0 += 4) {
+      const uint4 e4 = *reinterpret_cast<const uint4*>(edges + b0 + x0);
+      const uint32_t ee[4] = {e4.x, e4.y, e4.z, e4.w};
+      if (PACK) {
+        const uint4 r4 = *reinterpret_cast<const uint4*>(binR + b0 + x0);
+        const uint4 q4 = *reinterpret_cast<const uint4*>(binQ + b0 + x0);
+        const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w}, qq[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          bA[x0 + c] = (int)(rr[c] >> 9);
+          bN[x0 + c] = (int)(rr[c] & 511u);
+          qA[x0 + c] = (int)(qq[c] >> 9);
+          qN[x0 + c] = (int)(qq[c] & 511u);
+          ed[x0 + c] = ee[c];
+        }
+      } else {
+        const uint4 ra = *reinterpret_cast<const uint4*>(binR + b0 + x0);
+        const uint4 rn = *reinterpret_cast<const uint4*>(binR + NB + b0 + x0);
+        const uint4 qa = *reinterpret_cast<const uint4*>(binQ + b0 + x0);
+        const uint4 qn = *reinterpret_cast<const uint4*>(binQ + NB + b0 + x0);
+        const uint32_t a1[4] = {ra.x, ra.y, ra.z, ra.w}, n1[4] = {rn.x, rn.y, rn.z, rn.w};
+        const uint32_t a2[4] = {qa.x, qa.y, qa.z, qa.w}, n2[4] = {qn.x, qn.y, qn.z, qn.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          bA[x0 + c] = (int)a1[c];
+          bN[x0 + c] = (int)n1[c];
+          qA[x0 + c] = (int)a2[c];
+          qN[x0 + c] = (int)n2[c];
+          ed[x0 + c] = ee[c];
+        }
+      }
+    }
     int s[4] = {0, 0, 0, 0}, tot[4];
 #pragma unroll
     for (int x = 0; x < BPT; ++x) {
-      int A, N, Aq, Nq;
-      bin_an(binR, b0 + x, A, N);
-      bin_an(binQ, b0 + x, Aq, Nq);
-      s[0] += A;
-      s[1] += N;
-      s[2] += Aq;
-      s[3] += Nq;
+      s[0] += bA[x];
+      s[1] += bN[x];
+      s[2] += qA[x];
+      s[3] += qN[x];
     }
     T.template excl<4>(s, tot);
     const int s0[4] = {s[0], s[1], s[2], s[3]};
@@ -438,15 +516,11 @@ admit_kernel(AdmitParams p) {
     int lb_r = 0, lb_a = 0, lb_tau = 0, lb_trun = 0, ub_r = 0, ub_a = 0;
 #pragma unroll
     for (int x = 0; x < BPT; ++x) {
-      int A, N, Aq, Nq;
-      bin_an(binR, b0 + x, A, N);
-      bin_an(binQ, b0 + x, Aq, Nq);
-      s[0] += A;
-      s[1] += N;
-      s[2] += Aq;
-      s[3] += Nq;
-      const uint32_t ed = edges[b0 + x];
-      const int lo = (int)(ed & 0xFFFF), hi = (int)(ed >> 16);
+      s[0] += bA[x];
+      s[1] += bN[x];
+      s[2] += qA[x];
+      s[3] += qN[x];
+      const int lo = (int)(ed[x] & 0xFFFF), hi = (int)(ed[x] >> 16);
       const int vr = s[0] + lo * s[1];                    // T_R(lo)
       const int va = s[0] + s[2] + lo * (s[1] + s[3]);    // T_{R∪Q'}(lo)
       lb_r = ::max(lb_r, vr);
@@ -456,8 +530,8 @@ admit_kernel(AdmitParams p) {
         lb_trun = vr;
       }
       if (hi > lo) {  // wide bin: upper bounds where it holds requests
-        if (N > 0) ub_r = ::max(ub_r, s[0] + hi * s[1]);
-        if (N + Nq > 0) ub_a = ::max(ub_a, s[0] + s[2] + hi * (s[1] + s[3]));
+        if (bN[x] > 0) ub_r = ::max(ub_r, s[0] + hi * s[1]);
+        if (bN[x] + qN[x] > 0) ub_a = ::max(ub_a, s[0] + s[2] + hi * (s[1] + s[3]));
       }
     }
     Eval ev;
@@ -476,13 +550,10 @@ admit_kernel(AdmitParams p) {
     s[1] = s0[1];
     s[2] = s0[2];
     s[3] = s0[3];
-#pragma unroll 1
+#pragma unroll
     for (int x = 0; x < BPT; ++x) {
-      int A, N, Aq, Nq;
-      bin_an(binR, b0 + x, A, N);
-      bin_an(binQ, b0 + x, Aq, Nq);
-      const uint32_t ed = edges[b0 + x];
-      const int lo = (int)(ed & 0xFFFF), hi = (int)(ed >> 16);
+      const int A = bA[x], N = bN[x], Aq = qA[x], Nq = qN[x];
+      const int lo = (int)(ed[x] & 0xFFFF), hi = (int)(ed[x] >> 16);
       const bool c_r = need_r && N > 0 && hi > lo && s[0] + A + hi * (s[1] + N) > ev.m_run;
       const bool c_a = need_a && N + Nq > 0 && hi > lo &&
                        s[0] + A + s[2] + Aq + hi * (s[1] + N + s[3] + Nq) > ev.m_all;
@@ -490,7 +561,7 @@ admit_kernel(AdmitParams p) {
         const int slot = atomicAdd(&cand[0], 1);
         if (slot < 16) {
           int* cd = cand + 1 + 6 * slot;
-          cd[5] = (int)ed;  // lo | hi << 16
+          cd[5] = (int)ed[x];  // lo | hi << 16
           cd[0] = b0 + x;
           cd[1] = s[0];  // A_R, N_R, A_Q', N_Q' over the bins before b
           cd[2] = s[1];

@@ -53,17 +53,20 @@ const Variant kVariants[] = {PF_VARIANT(1, 512), PF_VARIANT(2, 1024), PF_VARIANT
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 inline int teams_per_cta(int TW) { return TW == 1 ? 4 : 1; }
 
-// Host copy of the kernel's log-linear bin map f(r) (pf_admit.cuh header): width-1
-// bins for r ≤ 16, 8 bins per octave up to width 2^s, then width 2^s.
+// Host copy of the kernel's log-linear bin map f(r) (pf_admit.cuh header), with
+// 2^KO sub-bins per octave (KO = log2(4·PF_BPT/2)): width-1 bins for r ≤ 2^(KO+1),
+// 2^KO bins per octave up to width 2^s, then width 2^s.
 int bin_f(int r, int s) {
-  if (r <= 16) return r - 1;
-  const int r0 = 1 << (s + 3);
+  const int KO = (PF_BPT == 2) ? 2 : (PF_BPT == 4) ? 3 : 4;
+  const int E = 2 << KO;
+  if (r <= E) return r - 1;
+  const int r0 = 1 << (s + KO);
   if (r < r0) {
     int o = 0;
     while ((2 << o) <= r) ++o;
-    return 16 + 8 * (o - 4) + ((r - (1 << o)) >> (o - 3));
+    return E + (1 << KO) * (o - KO - 1) + ((r - (1 << o)) >> (o - KO));
   }
-  return 16 + 8 * (s - 1) + ((r - r0) >> s);
+  return E + (1 << KO) * (s - 1) + ((r - r0) >> s);
 }
 
 }  // namespace
@@ -249,7 +252,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   for (int v = 0; v < kNumVariants; ++v)
     if (kVariants[v].cap >= C.max_entries) { c->variant = v; break; }
   const Variant& V = kVariants[c->variant];
-  c->n_bins = 128 * V.TW;
+  c->n_bins = 32 * PF_BPT * V.TW;
   c->bin_shift = 1;
   while (bin_f(C.max_len, c->bin_shift) > c->n_bins - 1) ++c->bin_shift;
   {  // r -> bin table and per-bin r ranges
