@@ -579,26 +579,32 @@ admit_kernel(AdmitParams p) {
     int best_r = ev.m_run, best_a = ev.m_all, best_tau = ev.tau, best_trun = ev.t_run;
     int vr = 0, va = 0, tau = 0, trun = 0;
     if (n_cand <= 16) {
-      // walk each candidate bin's request list: thread x takes the x-th included member
-      // and sums over the members with r ≥ its r (a second walk)
+      // walk each candidate bin's request list twice: the first walk hands the x-th
+      // included member to thread x, the second (all threads in step) accumulates,
+      // for each thread's member, the bin's members with r ≥ its r
       for (int c = 0; c < n_cand; ++c) {
         const int* cd = cand + 1 + 6 * c;
         const int head = (int)(hd[cd[0]] & 0xFFFFu);
-        int cnt = 0;
-        for (int e = head; e != 0xFFFF; e = nx[e]) {
-          if (e >= k && e - k + 1 > qlim) continue;  // queue request not in Q'
-          if ((cnt & (TT - 1)) == tid) {  // this thread's member: exact T at its r
-            const int rx = ent_r(e);
-            int Ar = cd[1], Nr = cd[2], Aa = cd[1] + cd[3], Na = cd[2] + cd[4];
-            for (int y = head; y != 0xFFFF; y = nx[y]) {
-              if (y >= k && y - k + 1 > qlim) continue;
-              const bool ge = ent_r(y) >= rx;
-              const int ay = ge ? ent_a(y) : 0;
-              Aa += ay;
-              Na += ge ? 1 : 0;
-              Ar += (y < k) ? ay : 0;
-              Nr += (ge && y < k) ? 1 : 0;
-            }
+        for (int round = 0;; round += TT) {
+          int cnt = 0, mine = -1;
+          for (int e = head; e != 0xFFFF; e = nx[e]) {
+            if (e >= k && e - k + 1 > qlim) continue;  // queue request not in Q'
+            if (cnt == round + tid) mine = e;
+            ++cnt;
+          }
+          if (cnt <= round) break;
+          const int rx = mine >= 0 ? ent_r(mine) : 0x7FFFFFFF;
+          int Ar = cd[1], Nr = cd[2], Aa = cd[1] + cd[3], Na = cd[2] + cd[4];
+          for (int y = head; y != 0xFFFF; y = nx[y]) {
+            if (y >= k && y - k + 1 > qlim) continue;
+            const bool ge = ent_r(y) >= rx;
+            const int ay = ge ? ent_a(y) : 0;
+            Aa += ay;
+            Na += ge ? 1 : 0;
+            Ar += (y < k) ? ay : 0;
+            Nr += (ge && y < k) ? 1 : 0;
+          }
+          if (mine >= 0) {
             const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;  // exact T at τ = rx
             vr = ::max(vr, t_r);
             if (t_a > va) {
@@ -607,7 +613,7 @@ admit_kernel(AdmitParams p) {
               trun = t_r;
             }
           }
-          ++cnt;
+          if (cnt <= round + TT) break;
         }
       }
     } else {
