@@ -620,27 +620,48 @@ admit_kernel(AdmitParams p) {
         }
       }
     } else {
-      // Pathological spread (> 16 candidate bins): exact T at every included request.
-      for (int ex = tid; ex < n_ent; ex += TT) {
-        if (ex >= k && ex - k + 1 > qlim) continue;
-        const int rx = ent_r(ex);
-        int Ar = 0, Nr = 0, Aa = 0, Na = 0;
-        for (int e = 0; e < n_ent; ++e) {
-          if (e >= k && e - k + 1 > qlim) continue;
-          const bool ge = ent_r(e) >= rx;
-          const int ae = ge ? ent_a(e) : 0;
-          Aa += ae;
-          Na += ge ? 1 : 0;
-          Ar += (e < k) ? ae : 0;
-          Nr += (ge && e < k) ? 1 : 0;
+      // Many candidate bins (large batches: the slack (hi − lo)·N is wide): every
+      // thread refines its own candidate bins, exactly, from their request lists and
+      // the prefix sums it already holds.
+      s[0] = s0[0];
+      s[1] = s0[1];
+      s[2] = s0[2];
+      s[3] = s0[3];
+#pragma unroll
+      for (int x = 0; x < BPT; ++x) {
+        const int A = bA[x], N = bN[x], Aq = qA[x], Nq = qN[x];
+        const int lo = (int)(ed[x] & 0xFFFF), hi = (int)(ed[x] >> 16);
+        const bool c_r = need_r && N > 0 && hi > lo && s[0] + A + hi * (s[1] + N) > ev.m_run;
+        const bool c_a = need_a && N + Nq > 0 && hi > lo &&
+                         s[0] + A + s[2] + Aq + hi * (s[1] + N + s[3] + Nq) > ev.m_all;
+        if (c_r || c_a) {
+          const int head = (int)(hd[b0 + x] & 0xFFFFu);
+          for (int e = head; e != 0xFFFF; e = nx[e]) {
+            if (e >= k && e - k + 1 > qlim) continue;  // queue request not in Q'
+            const int rx = ent_r(e);
+            int Ar = s[0], Nr = s[1], Aa = s[0] + s[2], Na = s[1] + s[3];
+            for (int y = head; y != 0xFFFF; y = nx[y]) {
+              if (y >= k && y - k + 1 > qlim) continue;
+              const bool ge = ent_r(y) >= rx;
+              const int ay = ge ? ent_a(y) : 0;
+              Aa += ay;
+              Na += ge ? 1 : 0;
+              Ar += (y < k) ? ay : 0;
+              Nr += (ge && y < k) ? 1 : 0;
+            }
+            const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;  // exact T at τ = rx
+            vr = ::max(vr, t_r);
+            if (t_a > va) {
+              va = t_a;
+              tau = rx;
+              trun = t_r;
+            }
+          }
         }
-        const int t_r = Ar + rx * Nr, t_a = Aa + rx * Na;
-        vr = ::max(vr, t_r);
-        if (t_a > va) {
-          va = t_a;
-          tau = rx;
-          trun = t_r;
-        }
+        s[0] += A;
+        s[1] += N;
+        s[2] += Aq;
+        s[3] += Nq;
       }
     }
     best_r = ::max(best_r, T.max(vr));
