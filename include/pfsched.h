@@ -89,7 +89,8 @@ enum {
   PF_DERR_MAX_NEW = 3,     /* max_new ∉ [1, Lmax]                                       */
   PF_DERR_INPUT_LEN = 4,   /* l_p ∉ [0, max_input_len]                                  */
   PF_DERR_GENERATED = 5,   /* l_t ∉ [0, max_new − 1]                                    */
-  PF_DERR_CAPACITY = 6     /* capacity < 0                                              */
+  PF_DERR_CAPACITY = 6,    /* capacity < 0                                              */
+  PF_DERR_OVERRIDE = 7     /* pf_admit_override: l̂ ∉ (l_t, Lmax] (running) or [1, Lmax] */
 };
 
 typedef struct {
@@ -172,6 +173,19 @@ pf_status pf_admit(pf_ctx* ctx, const int32_t* run_off, const int32_t* input_len
                    const int32_t* max_new, const int32_t* capacity, uint32_t tick,
                    int32_t* admitted_out, int32_t* peak_out, int32_t* peak_running_out,
                    int32_t* pred_run_out, int32_t* pred_q_out, void* stream);
+
+/* Theoretical optimum (PAPER.md:341 "Theoretical optimum", :395: "the memory is
+ * optimally utilized when the request output length is known"): Algorithm 1's
+ * admission and Eq.(eq:1)-(eq:3) with the caller's l̂ per request instead of the
+ * prediction (e.g. true output lengths). lhat_run: [run_off[n]], l_t < l̂ ≤ Lmax;
+ * lhat_q: [q_off[n]], 1 ≤ l̂ ≤ Lmax; no max_new clamp. Outputs as pf_admit.
+ * Violations give PF_DERR_OVERRIDE and −1 outputs for the instance. */
+pf_status pf_admit_override(pf_ctx* ctx, const int32_t* run_off, const int32_t* input_len,
+                            const int32_t* generated, const int32_t* lhat_run,
+                            const int32_t* q_off, const int32_t* q_input_len,
+                            const int32_t* lhat_q, const int32_t* capacity,
+                            int32_t* admitted_out, int32_t* peak_out,
+                            int32_t* peak_running_out, void* stream);
 
 /* Read (and keep) the sticky device error word; synchronises `stream`. */
 pf_status pf_get_device_error(pf_ctx* ctx, int32_t* code, int32_t* index, void* stream);

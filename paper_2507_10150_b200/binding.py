@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libpfsched.so")
 
 PF_MODE_SAMPLE, PF_MODE_QUANTILE = 0, 1
 DERR = {0: "none", 1: "completion", 2: "offsets", 3: "max_new", 4: "input_len", 5: "generated",
-        6: "capacity"}
+        6: "capacity", 7: "override"}
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -36,8 +36,8 @@ class PFConfig(ctypes.Structure):
 
 _lib = None
 SYMBOLS = ("pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer", "pf_commit_history",
-           "pf_estimate_peak", "pf_admit", "pf_get_device_error", "pf_clear_device_error",
-           "pf_export_history", "pf_last_error", "pf_abi_version")
+           "pf_estimate_peak", "pf_admit", "pf_admit_override", "pf_get_device_error",
+           "pf_clear_device_error", "pf_export_history", "pf_last_error", "pf_abi_version")
 
 
 def load(path: str = LIB_PATH):
@@ -58,6 +58,7 @@ def load(path: str = LIB_PATH):
     L.pf_commit_history.argtypes = [_vp, _vp]
     L.pf_estimate_peak.argtypes = [_vp, _vp, _vp, _vp, _vp, ctypes.c_uint32, _vp, _vp, _vp]
     L.pf_admit.argtypes = [_vp] + [_vp] * 7 + [ctypes.c_uint32] + [_vp] * 6
+    L.pf_admit_override.argtypes = [_vp] * 13
     L.pf_get_device_error.argtypes = [_vp, P(_i32), P(_i32), _vp]
     L.pf_clear_device_error.argtypes = [_vp, _vp]
     L.pf_export_history.argtypes = [_vp, _vp, _vp]
@@ -160,6 +161,20 @@ class Scheduler:
                                _ptr(q_input_len), _ptr(max_new), _ptr(capacity), tick & 0xFFFFFFFF,
                                _ptr(admitted_out), _ptr(peak_out), _ptr(peak_running_out),
                                _ptr(pred_run_out), _ptr(pred_q_out), _stream()), "pf_admit")
+        return admitted_out, peak_out
+
+    def admit_override(self, run_off, input_len, generated, lhat_run, q_off, q_input_len, lhat_q, capacity,
+                       *, admitted_out=None, peak_out=None, peak_running_out=None):
+        """A12 theoretical optimum: Alg.1 with the caller's l̂ (e.g. true output lengths)."""
+        dev = run_off.device
+        if admitted_out is None:
+            admitted_out = torch.empty(self.n, dtype=torch.int32, device=dev)
+        if peak_out is None:
+            peak_out = torch.empty(self.n, dtype=torch.int32, device=dev)
+        _check(load().pf_admit_override(self._h, _ptr(run_off), _ptr(input_len), _ptr(generated),
+                                        _ptr(lhat_run), _ptr(q_off), _ptr(q_input_len), _ptr(lhat_q),
+                                        _ptr(capacity), _ptr(admitted_out), _ptr(peak_out),
+                                        _ptr(peak_running_out), _stream()), "pf_admit_override")
         return admitted_out, peak_out
 
     def device_error(self):

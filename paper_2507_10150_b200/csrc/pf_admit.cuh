@@ -79,6 +79,10 @@ struct AdmitParams {
   int32_t* pred_run_out;
   int32_t* pred_q_out;
   int32_t* err;
+  // A12 theoretical optimum: caller-supplied l̂ replaces the
+  // prediction (nullable; when set, max_new may be NULL and no clamp applies)
+  const int32_t* lhat_run;   // [run_off[n]]
+  const int32_t* lhat_q;     // [q_off[n]]
 };
 
 // #{x in S[0..w) : x <= v} for ascending S (upper_bound).
@@ -240,7 +244,7 @@ admit_kernel(AdmitParams p) {
   const int q0 = estimate_only ? 0 : p.q_off[i];
   const int q1 = estimate_only ? 0 : p.q_off[i + 1];
   const int k = r1 - r0, q = q1 - q0, n_ent = k + q;
-  const int max_new = p.max_new[i];
+  const int max_new = p.max_new ? p.max_new[i] : p.max_len;
   const int cap = estimate_only ? 0 : p.capacity[i];
   int bad = 0;
   if (k < 0 || q < 0 || n_ent > p.max_entries) bad = PF_BAD_OFFSETS;
@@ -320,8 +324,9 @@ admit_kernel(AdmitParams p) {
     return draw_u(key_fold, e, p.R);
   };
   // l̂ → r, a; bin; push; (A, N) into the running or queue bins
+  const bool override_lhat = p.lhat_run != nullptr;
   auto finish = [&](int e, int l_hat, int l_t, int l_p, bool run) {
-    l_hat = ::min(l_hat, max_new);  // C-6
+    if (!override_lhat) l_hat = ::min(l_hat, max_new);  // C-6
     if (want_pred) {
       int32_t* pout = run ? p.pred_run_out : p.pred_q_out;
       if (pout) pout[run ? r0 + e : q0 - k + e] = l_hat;
@@ -345,6 +350,25 @@ admit_kernel(AdmitParams p) {
     }
   };
   // running requests e ∈ [0, k): l̂ from P(l > l_t)
+  if (override_lhat) {
+    // A12: l̂ given per request; need l_t < l̂ ≤ Lmax (running), 1 ≤ l̂ ≤ Lmax (queued)
+#pragma unroll 1
+    for (int e = tid; e < k; e += TT) {
+      const int l_p = __ldg(p.input_len + r0 + e), l_t = __ldg(p.generated + r0 + e);
+      const int l_hat = __ldg(p.lhat_run + r0 + e);
+      const bool bad = (unsigned)l_p > (unsigned)p.max_input_len || l_t < 0 || l_hat <= l_t ||
+                       l_hat > p.max_len;
+      my_bad |= bad;
+      if (!bad) finish(e, l_hat, l_t, l_p, true);
+    }
+#pragma unroll 1
+    for (int j = tid; j < q; j += TT) {
+      const int l_p = __ldg(p.q_input_len + q0 + j), l_hat = __ldg(p.lhat_q + q0 + j);
+      const bool bad = (unsigned)l_p > (unsigned)p.max_input_len || l_hat < 1 || l_hat > p.max_len;
+      my_bad |= bad;
+      if (!bad) finish(k + j, l_hat, 0, l_p, false);
+    }
+  } else {
   const int32_t* lp_base = p.input_len + r0;
   const int32_t* lt_base = p.generated + r0;
 #pragma unroll 1
@@ -431,12 +455,14 @@ admit_kernel(AdmitParams p) {
       if (j < q) finish(k + j, lh[c], 0, lp[c], false);
     }
   }
+  }  // !override_lhat
   if (T.any(my_bad != 0)) {
     // Data-dependent violation: outputs of this instance are −1.
     for (int e = tid; e < n_ent; e += TT) {
       const int l_p = e < k ? p.input_len[r0 + e] : p.q_input_len[q0 + (e - k)];
       const int l_t = e < k ? p.generated[r0 + e] : 0;
       if (l_p < 0 || l_p > p.max_input_len) raise_error(p.err, PF_BAD_INPUT_LEN, i);
+      else if (override_lhat) raise_error(p.err, PF_BAD_OVERRIDE, i);
       else if (l_t < 0 || l_t >= max_new) raise_error(p.err, PF_BAD_GENERATED, i);
     }
     for (int e = tid; e < n_ent; e += TT) {

@@ -10,7 +10,7 @@ constexpr int kWarp = 32;
 
 // Device error codes (mirror PF_DERR_* of include/pfsched.h).
 enum { PF_BAD_COMPLETION = 1, PF_BAD_OFFSETS = 2, PF_BAD_MAX_NEW = 3, PF_BAD_INPUT_LEN = 4,
-       PF_BAD_GENERATED = 5, PF_BAD_CAPACITY = 6 };
+       PF_BAD_GENERATED = 5, PF_BAD_CAPACITY = 6, PF_BAD_OVERRIDE = 7 };
 
 // ---------------------------------------------------------------- C-8 hash
 // SplitMix64 finalizer and lowbias32 (DESIGN.md §3 C-8; include/pfsched.h "u").

@@ -347,7 +347,8 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
                               const int32_t* q_input_len, const int32_t* max_new,
                               const int32_t* capacity, uint32_t tick, int32_t* admitted_out,
                               int32_t* peak_out, int32_t* peak_running_out, int32_t* pred_run_out,
-                              int32_t* pred_q_out, cudaStream_t s) {
+                              int32_t* pred_q_out, cudaStream_t s,
+                              const int32_t* lhat_run = nullptr, const int32_t* lhat_q = nullptr) {
   const pf_config& C = c->cfg;
   pf::AdmitParams p;
   memset(&p, 0, sizeof(p));
@@ -389,6 +390,8 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.peak_running_out = peak_running_out;
   p.pred_run_out = pred_run_out;
   p.pred_q_out = pred_q_out;
+  p.lhat_run = lhat_run;
+  p.lhat_q = lhat_q;
   p.err = c->err;
   const Variant& V = kVariants[c->variant];
   const int teams = teams_per_cta(V.TW);
@@ -418,6 +421,20 @@ pf_status pf_admit(pf_ctx* c, const int32_t* run_off, const int32_t* input_len,
   return launch_admit(c, run_off, input_len, generated, q_off, q_input_len, max_new, capacity,
                       tick, admitted_out, peak_out, peak_running_out, pred_run_out, pred_q_out,
                       S(stream));
+}
+
+pf_status pf_admit_override(pf_ctx* c, const int32_t* run_off, const int32_t* input_len,
+                            const int32_t* generated, const int32_t* lhat_run,
+                            const int32_t* q_off, const int32_t* q_input_len,
+                            const int32_t* lhat_q, const int32_t* capacity,
+                            int32_t* admitted_out, int32_t* peak_out,
+                            int32_t* peak_running_out, void* stream) {
+  if (!c || !run_off || !input_len || !generated || !lhat_run || !q_off || !q_input_len ||
+      !lhat_q || !capacity || !admitted_out || !peak_out)
+    return fail(PF_EINVAL, "pf_admit_override: NULL required pointer");
+  return launch_admit(c, run_off, input_len, generated, q_off, q_input_len, nullptr, capacity, 0,
+                      admitted_out, peak_out, peak_running_out, nullptr, nullptr, S(stream),
+                      lhat_run, lhat_q);
 }
 
 pf_status pf_get_device_error(pf_ctx* c, int32_t* code, int32_t* index, void* stream) {
