@@ -289,9 +289,26 @@ admit_kernel(AdmitParams p) {
 #pragma unroll
     for (int x = 0; x < NB / 4 / TT; ++x) h4[tid + x * TT] = make_uint4(~0u, ~0u, ~0u, ~0u);
   }
+  // LOOK_SORTED coarse index over the sorted window: cidx[c] = #{S < c·2^csh}, c ≤ 64,
+  // so upper_bound(S, l) is a binary search inside [cidx[l >> csh], cidx[(l >> csh) + 1]).
+  int* cidx = table + w;
+  int csh = 0;
+  while (((p.max_len + 1) >> csh) > 64) ++csh;
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
     for (int x = tid; x < w; x += TT) table[x] = __ldg(src + x);
+    T.sync();
+    for (int c = tid; c <= 65; c += TT) {
+      const int v = c << csh;  // lower_bound(S, v)
+      int lo = 0, len = w;
+      while (len > 0) {
+        const int half = len >> 1;
+        const bool right = table[lo + half] < v;
+        lo = right ? lo + half + 1 : lo;
+        len = right ? len - half - 1 : half;
+      }
+      cidx[c] = (c == 65) ? w : lo;
+    }
   } else if (LOOK == LOOK_HIST) {
     // C[l] = #{h ∈ L_h : h ≤ l}: inclusive scan of the persistent histogram.
     const int nb = p.max_len + 1;
@@ -393,7 +410,15 @@ admit_kernel(AdmitParams p) {
       u[c] = draw(e);
       if (LOOK == LOOK_GROUP) bq[c] = __ldg(gC + lt[c]);
       else if (LOOK == LOOK_HIST) bq[c] = table[lt[c]];
-      else bq[c] = upper_bound_smem(table, w, lt[c]);
+      else {  // #{S ≤ l_t}: first S > l_t inside the coarse bucket of l_t
+        const int cb = lt[c] >> csh;
+        int lo = cidx[cb], hi = cidx[cb + 1];
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (table[mid] <= lt[c]) lo = mid + 1; else hi = mid;
+        }
+        bq[c] = lo;
+      }
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
