@@ -33,6 +33,22 @@
 #ifndef PF_BPT
 #define PF_BPT 4
 #endif
+// Refinement strategy switch: up to this many candidate bins the whole team walks each
+// candidate's list in lock-step; beyond it every thread refines its own candidate bins.
+#ifndef PF_LOCKSTEP_MAX
+#define PF_LOCKSTEP_MAX 16
+#endif
+// Track the smallest / largest r present in each bin (over all requests of the
+// instance) to tighten the bin bounds: lo_b = min r, hi_b = max r (exact T at the min;
+// bins holding one distinct r need no refinement). Pays off for multi-warp teams (large
+// instances); for one-warp teams the extra shared memory costs more L1 than it saves.
+#ifndef PF_MINMAX
+#define PF_MINMAX 1
+#endif
+template <int TW>
+struct MinMax {
+  static constexpr bool on = PF_MINMAX && TW > 1;
+};
 
 namespace pf {
 
@@ -226,7 +242,9 @@ admit_kernel(AdmitParams p) {
   int* av = reinterpret_cast<int*>(rb + p.ent_cap);  // unused when PACK
   uint16_t* nx = reinterpret_cast<uint16_t*>(av + (PACK ? 0 : p.ent_cap));
   uint32_t* hd = reinterpret_cast<uint32_t*>(nx + p.ent_cap);
-  uint32_t* binR = hd + NB;
+  uint32_t* rmn = hd + NB;                 // [NB] min r per bin (PF_MINMAX)
+  uint32_t* rmx = rmn + (MinMax<TW>::on ? NB : 0);  // [NB] max r per bin
+  uint32_t* binR = rmx + (MinMax<TW>::on ? NB : 0);
   uint32_t* binQ = binR + NBW;
   T.xs = reinterpret_cast<int*>(binQ + NBW);
   int* cand = T.xs + 40;    // [0]: count, then 6 ints per candidate (≤ 16); xs[36]: list size
@@ -288,6 +306,15 @@ admit_kernel(AdmitParams p) {
     uint4* h4 = reinterpret_cast<uint4*>(hd);  // empty lists
 #pragma unroll
     for (int x = 0; x < NB / 4 / TT; ++x) h4[tid + x * TT] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (MinMax<TW>::on) {
+      uint4* n4 = reinterpret_cast<uint4*>(rmn);
+      uint4* x4 = reinterpret_cast<uint4*>(rmx);
+#pragma unroll
+      for (int x = 0; x < NB / 4 / TT; ++x) {
+        n4[tid + x * TT] = make_uint4(0xFFFFu, 0xFFFFu, 0xFFFFu, 0xFFFFu);
+        x4[tid + x * TT] = make_uint4(0, 0, 0, 0);
+      }
+    }
   }
   // LOOK_SORTED coarse index over the sorted window: cidx[c] = #{S < c·2^csh}, c ≤ 64,
   // so upper_bound(S, l) is a binary search inside [cidx[l >> csh], cidx[(l >> csh) + 1]).
@@ -358,6 +385,10 @@ admit_kernel(AdmitParams p) {
       av[e] = a;
     }
     nx[e] = (uint16_t)atomicExch(&hd[b], (uint32_t)e);  // push onto bin b's list
+    if (MinMax<TW>::on) {
+      atomicMin(&rmn[b], (uint32_t)r);
+      atomicMax(&rmx[b], (uint32_t)r);
+    }
     uint32_t* bins = run ? binR : binQ;
     if (PACK) {
       atomicAdd(&bins[b], ((uint32_t)a << 9) | 1u);
@@ -526,7 +557,15 @@ admit_kernel(AdmitParams p) {
 #pragma unroll
     for (int x0 = 0; x0 < BPT; x0 += 4) {
       const uint4 e4 = *reinterpret_cast<const uint4*>(edges + b0 + x0);
-      const uint32_t ee[4] = {e4.x, e4.y, e4.z, e4.w};
+      uint32_t ee[4] = {e4.x, e4.y, e4.z, e4.w};
+      if (MinMax<TW>::on) {  // actual r range of the bin's requests (when it has any)
+        const uint4 n4 = *reinterpret_cast<const uint4*>(rmn + b0 + x0);
+        const uint4 m4 = *reinterpret_cast<const uint4*>(rmx + b0 + x0);
+        const uint32_t nn[4] = {n4.x, n4.y, n4.z, n4.w}, mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (mm[c] != 0) ee[c] = nn[c] | (mm[c] << 16);
+      }
       if (PACK) {
         const uint4 r4 = *reinterpret_cast<const uint4*>(binR + b0 + x0);
         const uint4 q4 = *reinterpret_cast<const uint4*>(binQ + b0 + x0);
@@ -632,7 +671,7 @@ admit_kernel(AdmitParams p) {
     const int n_cand = cand[0];
     int best_r = ev.m_run, best_a = ev.m_all, best_tau = ev.tau, best_trun = ev.t_run;
     int vr = 0, va = 0, tau = 0, trun = 0;
-    if (n_cand <= 16) {
+    if (n_cand <= PF_LOCKSTEP_MAX) {  // few candidates: all threads on each in turn
       // walk each candidate bin's request list twice: the first walk hands the x-th
       // included member to thread x, the second (all threads in step) accumulates,
       // for each thread's member, the bin's members with r ≥ its r

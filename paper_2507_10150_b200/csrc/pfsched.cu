@@ -8,7 +8,7 @@
 #include <vector>
 
 #include "../../include/pfsched.h"
-#include "pf_admit.cuh"
+#include "pf_admit.cuh"  // defines PF_BPT, PF_MINMAX, PF_LOCKSTEP_MAX
 #include "pf_history.cuh"
 
 namespace {
@@ -279,8 +279,8 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
   c->ent_cap = (C.max_entries + 7) & ~7;
   const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
-  size_t team = (size_t)c->ent_cap * (c->pack ? 6 : 10) + (size_t)c->n_bins * 4 + nbw * 8 +
-                160 * 4 + table;
+  size_t team = (size_t)c->ent_cap * (c->pack ? 6 : 10) + (size_t)c->n_bins * 4 * ((PF_MINMAX && V.TW > 1) ? 3 : 1) +
+                nbw * 8 + 160 * 4 + table;
   team = (team + 15) & ~(size_t)15;
   c->team_smem = (int)team;
   c->admit_smem = (size_t)c->n_bins * 4 + team * teams_per_cta(V.TW);
