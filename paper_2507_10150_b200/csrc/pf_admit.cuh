@@ -549,7 +549,10 @@ admit_kernel(AdmitParams p) {
       N = (int)bins[NB + b];
     }
   };
-  auto evaluate = [&](int qlim) -> Eval {
+  // first = the evaluation whose m_run is reported (M*(R)); m_all needs to be exact only
+  // when it can be the reported peak (≤ C): above C, the bin attaining the largest exact
+  // lower bound already gives a violating τ for the cutting plane.
+  auto evaluate = [&](int qlim, bool first) -> Eval {
     const int b0 = tid * BPT;
     // this thread's bins in registers (16-byte shared loads)
     int bA[BPT], bN[BPT], qA[BPT], qN[BPT];
@@ -633,8 +636,8 @@ admit_kernel(AdmitParams p) {
     ev.tau = lb_tau;
     ev.t_run = lb_trun;
     T.pick(lb_a == ev.m_all, ev.tau, ev.t_run);
-    const bool need_r = T.max(ub_r) > ev.m_run;
-    const bool need_a = T.max(ub_a) > ev.m_all;
+    const bool need_r = first && T.max(ub_r) > ev.m_run;
+    const bool need_a = !estimate_only && ev.m_all <= Cmax && T.max(ub_a) > ev.m_all;
     if (!need_r && !need_a) return ev;
     // ---- refinement of the wide bins whose upper bound beats the current maximum
     if (tid == 0) cand[0] = 0;
@@ -775,7 +778,7 @@ admit_kernel(AdmitParams p) {
   int p_star = 0, peak = 0, M0 = 0, ph = q;
   bool first = true;
   for (;;) {
-    const Eval ev = evaluate(ph);
+    const Eval ev = evaluate(ph, first);
     if (first) {
       first = false;
       M0 = ev.m_run;  // Eq.(eq:3): M*(R)
