@@ -80,6 +80,7 @@ typedef enum {
 } pf_status;
 
 enum { PF_MODE_SAMPLE = 0, PF_MODE_QUANTILE = 1 };
+enum { PF_POLICY_AGGRESSIVE = 1, PF_POLICY_CONSERVATIVE = 2 };
 
 /* Device error codes (sticky word, see pf_get_device_error). */
 enum {
@@ -186,6 +187,21 @@ pf_status pf_admit_override(pf_ctx* ctx, const int32_t* run_off, const int32_t* 
                             const int32_t* lhat_q, const int32_t* capacity,
                             int32_t* admitted_out, int32_t* peak_out,
                             int32_t* peak_running_out, void* stream);
+
+/* The paper's comparison policies (§5.3 Table 1),
+ * batched on the same inputs, FIFO with early return:
+ *   PF_POLICY_AGGRESSIVE   (watermark): admit the queue head while
+ *       10^4·(Σ_running(l_p + l_t) + Σ_admitted l_p) ≤ ratio_bp·M
+ *   PF_POLICY_CONSERVATIVE (overcommit, ":379 assumes 1.5 times"): admit while
+ *       10^4·Σ_{running ∪ admitted}(l_p + max_new) ≤ ratio_bp·M
+ * ratio_bp ≥ 1 (e.g. 9500 = watermark 95 %, 15000 = overcommit 150 %). Outputs:
+ * admitted_out [n] = p*, used_out nullable [n] = the left-hand sum for the admitted set.
+ * Validation and −1 outputs as pf_admit. Needs no history. */
+pf_status pf_admit_baseline(pf_ctx* ctx, int32_t policy, int32_t ratio_bp, const int32_t* run_off,
+                            const int32_t* input_len, const int32_t* generated,
+                            const int32_t* q_off, const int32_t* q_input_len,
+                            const int32_t* max_new, const int32_t* capacity,
+                            int32_t* admitted_out, int32_t* used_out, void* stream);
 
 /* Read (and keep) the sticky device error word; synchronises `stream`. */
 pf_status pf_get_device_error(pf_ctx* ctx, int32_t* code, int32_t* index, void* stream);

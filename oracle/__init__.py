@@ -93,6 +93,12 @@ def lib():
         L.orc_admit.restype = ctypes.c_int32
         L.orc_admit.argtypes = [ctypes.c_void_p, ctypes.POINTER(_AdmitArgs), ctypes.c_int32]
         L.orc_sizeof_admit_args.restype = ctypes.c_int32
+        L.orc_admit_aggressive.restype = ctypes.c_int32
+        L.orc_admit_aggressive.argtypes = [ctypes.c_int32, I32P, I32P, ctypes.c_int32, I32P, ctypes.c_int64,
+                                           ctypes.c_int32, I64P]
+        L.orc_admit_conservative.restype = ctypes.c_int32
+        L.orc_admit_conservative.argtypes = [ctypes.c_int32, I32P, ctypes.c_int32, I32P, ctypes.c_int32,
+                                             ctypes.c_int64, ctypes.c_int32, I64P]
         assert L.orc_sizeof_admit_args() == ctypes.sizeof(_AdmitArgs), "oracle ABI struct mismatch"
         _lib = L
     return _lib
@@ -164,6 +170,24 @@ def admit_one_bsearch(run_a, run_r, q_a, q_r, capacity: int, bp: int = 0):
     p = lib().orc_admit_one_bsearch(len(ra), _p32(ra), _p32(rr), len(qa), _p32(qa), _p32(qr),
                                     capacity, bp, ctypes.byref(pk))
     return p, pk.value
+
+
+def admit_aggressive(run_lp, run_lt, q_lp, capacity: int, watermark_bp: int):
+    """Baseline: watermark admission on input lengths only -> (p*, used)."""
+    a, b, c = _i32(run_lp), _i32(run_lt), _i32(q_lp)
+    used = ctypes.c_int64()
+    p = lib().orc_admit_aggressive(len(a), _p32(a), _p32(b), len(c), _p32(c), capacity, watermark_bp,
+                                   ctypes.byref(used))
+    return p, used.value
+
+
+def admit_conservative(run_lp, q_lp, max_new: int, capacity: int, overcommit_bp: int):
+    """Baseline: input + max_new budget admission -> (p*, used)."""
+    a, c = _i32(run_lp), _i32(q_lp)
+    used = ctypes.c_int64()
+    p = lib().orc_admit_conservative(len(a), _p32(a), len(c), _p32(c), max_new, capacity, overcommit_bp,
+                                     ctypes.byref(used))
+    return p, used.value
 
 
 # ---------------------------------------------------------------- batched

@@ -444,4 +444,51 @@ int32_t orc_admit(const orc_ctx* c, const orc_admit_args* A, int32_t n_threads) 
 
 int32_t orc_sizeof_admit_args(void) { return (int32_t)sizeof(orc_admit_args); }
 
+// ---------------------------------------------------------------------------
+// Baseline admission policies the paper compares against (§5.3
+// Table 1 rows :345-349), one instance, FIFO with early return:
+//   aggressive   (watermark, "batches requests solely based on
+//                input lengths"): admit the j-th queued request while
+//                Σ_running(l_p + l_t) + Σ_{admitted ∪ j} l_p ≤ watermark·M
+//   conservative (overcommit, "the sum of request input lengths and
+//                the max_new_tokens", :379 "assumes 1.5 times the memory"): admit while
+//                Σ_{running ∪ admitted ∪ j}(l_p + max_new) ≤ overcommit·M
+// Ratios in basis points; compare 10^4·used ≤ ratio_bp·M in int64. Returns p*;
+// *used = the left-hand side for the admitted set.
+int32_t orc_admit_aggressive(int32_t k, const int32_t* run_lp, const int32_t* run_lt, int32_t q,
+                             const int32_t* q_lp, int64_t capacity, int32_t watermark_bp,
+                             int64_t* used) {
+  int64_t consumed = 0;
+  for (int32_t s = 0; s < k; ++s) consumed += (int64_t)run_lp[s] + run_lt[s];
+  int32_t admitted = 0;
+  for (int32_t j = 0; j < q; ++j) {
+    if ((consumed + q_lp[j]) * 10000 <= (int64_t)watermark_bp * capacity) {
+      consumed += q_lp[j];
+      admitted = j + 1;
+    } else {
+      break;
+    }
+  }
+  if (used) *used = consumed;
+  return admitted;
+}
+
+int32_t orc_admit_conservative(int32_t k, const int32_t* run_lp, int32_t q, const int32_t* q_lp,
+                               int32_t max_new, int64_t capacity, int32_t overcommit_bp,
+                               int64_t* used) {
+  int64_t budget = 0;
+  for (int32_t s = 0; s < k; ++s) budget += (int64_t)run_lp[s] + max_new;
+  int32_t admitted = 0;
+  for (int32_t j = 0; j < q; ++j) {
+    if ((budget + q_lp[j] + max_new) * 10000 <= (int64_t)overcommit_bp * capacity) {
+      budget += (int64_t)q_lp[j] + max_new;
+      admitted = j + 1;
+    } else {
+      break;
+    }
+  }
+  if (used) *used = budget;
+  return admitted;
+}
+
 }  // extern "C"

@@ -5,8 +5,8 @@ and FIFO admission over many independent scheduler instances.
 The computation lives in libpfsched.so (CUDA kernels behind the C-ABI declared in
 include/pfsched.h); ``binding`` is a ctypes marshalling layer with the same names.
 """
-from .binding import (PF_MODE_QUANTILE, PF_MODE_SAMPLE, PFError, Scheduler, load, LIB_PATH,
-                      SYMBOLS)
+from .binding import (PF_MODE_QUANTILE, PF_MODE_SAMPLE, PF_POLICY_AGGRESSIVE, PF_POLICY_CONSERVATIVE,
+                      PFError, Scheduler, load, LIB_PATH, SYMBOLS)
 
 __all__ = ["Scheduler", "PFError", "load", "LIB_PATH", "SYMBOLS", "PF_MODE_SAMPLE",
-           "PF_MODE_QUANTILE"]
+           "PF_MODE_QUANTILE", "PF_POLICY_AGGRESSIVE", "PF_POLICY_CONSERVATIVE"]

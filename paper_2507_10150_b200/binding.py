@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpfsched.so")
 
 PF_MODE_SAMPLE, PF_MODE_QUANTILE = 0, 1
+PF_POLICY_AGGRESSIVE, PF_POLICY_CONSERVATIVE = 1, 2
 DERR = {0: "none", 1: "completion", 2: "offsets", 3: "max_new", 4: "input_len", 5: "generated",
         6: "capacity", 7: "override"}
 
@@ -36,7 +37,7 @@ class PFConfig(ctypes.Structure):
 
 _lib = None
 SYMBOLS = ("pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer", "pf_commit_history",
-           "pf_estimate_peak", "pf_admit", "pf_admit_override", "pf_get_device_error",
+           "pf_estimate_peak", "pf_admit", "pf_admit_override", "pf_admit_baseline", "pf_get_device_error",
            "pf_clear_device_error", "pf_export_history", "pf_last_error", "pf_abi_version")
 
 
@@ -59,6 +60,7 @@ def load(path: str = LIB_PATH):
     L.pf_estimate_peak.argtypes = [_vp, _vp, _vp, _vp, _vp, ctypes.c_uint32, _vp, _vp, _vp]
     L.pf_admit.argtypes = [_vp] + [_vp] * 7 + [ctypes.c_uint32] + [_vp] * 6
     L.pf_admit_override.argtypes = [_vp] * 13
+    L.pf_admit_baseline.argtypes = [_vp, _i32, _i32] + [_vp] * 10
     L.pf_get_device_error.argtypes = [_vp, P(_i32), P(_i32), _vp]
     L.pf_clear_device_error.argtypes = [_vp, _vp]
     L.pf_export_history.argtypes = [_vp, _vp, _vp]
@@ -176,6 +178,20 @@ class Scheduler:
                                         _ptr(capacity), _ptr(admitted_out), _ptr(peak_out),
                                         _ptr(peak_running_out), _stream()), "pf_admit_override")
         return admitted_out, peak_out
+
+    def admit_baseline(self, policy: int, ratio_bp: int, run_off, input_len, generated, q_off, q_input_len,
+                       max_new, capacity, *, admitted_out=None, used_out=None):
+        """The paper's aggressive (watermark) / conservative (overcommit) admission policies."""
+        dev = run_off.device
+        if admitted_out is None:
+            admitted_out = torch.empty(self.n, dtype=torch.int32, device=dev)
+        if used_out is None:
+            used_out = torch.empty(self.n, dtype=torch.int32, device=dev)
+        _check(load().pf_admit_baseline(self._h, policy, ratio_bp, _ptr(run_off), _ptr(input_len),
+                                        _ptr(generated), _ptr(q_off), _ptr(q_input_len), _ptr(max_new),
+                                        _ptr(capacity), _ptr(admitted_out), _ptr(used_out), _stream()),
+               "pf_admit_baseline")
+        return admitted_out, used_out
 
     def device_error(self):
         code, idx = _i32(), _i32()

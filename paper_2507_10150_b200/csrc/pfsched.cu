@@ -9,6 +9,7 @@
 
 #include "../../include/pfsched.h"
 #include "pf_admit.cuh"  // defines PF_BPT, PF_MINMAX, PF_LOCKSTEP_MAX
+#include "pf_baseline.cuh"
 #include "pf_history.cuh"
 
 namespace {
@@ -435,6 +436,40 @@ pf_status pf_admit_override(pf_ctx* c, const int32_t* run_off, const int32_t* in
   return launch_admit(c, run_off, input_len, generated, q_off, q_input_len, nullptr, capacity, 0,
                       admitted_out, peak_out, peak_running_out, nullptr, nullptr, S(stream),
                       lhat_run, lhat_q);
+}
+
+pf_status pf_admit_baseline(pf_ctx* c, int32_t policy, int32_t ratio_bp, const int32_t* run_off,
+                            const int32_t* input_len, const int32_t* generated,
+                            const int32_t* q_off, const int32_t* q_input_len,
+                            const int32_t* max_new, const int32_t* capacity,
+                            int32_t* admitted_out, int32_t* used_out, void* stream) {
+  if (!c || !run_off || !input_len || !generated || !q_off || !q_input_len || !max_new ||
+      !capacity || !admitted_out)
+    return fail(PF_EINVAL, "pf_admit_baseline: NULL required pointer");
+  if (policy != PF_POLICY_AGGRESSIVE && policy != PF_POLICY_CONSERVATIVE)
+    return fail(PF_EINVAL, "pf_admit_baseline: unknown policy %d", policy);
+  if (ratio_bp < 1) return fail(PF_EINVAL, "pf_admit_baseline: ratio_bp must be >= 1");
+  pf::BaselineParams p;
+  p.n = c->cfg.n_instances;
+  p.policy = policy;
+  p.ratio_bp = ratio_bp;
+  p.max_len = c->cfg.max_len;
+  p.max_input_len = c->cfg.max_input_len;
+  p.max_entries = c->cfg.max_entries;
+  p.run_off = run_off;
+  p.input_len = input_len;
+  p.generated = generated;
+  p.q_off = q_off;
+  p.q_input_len = q_input_len;
+  p.max_new = max_new;
+  p.capacity = capacity;
+  p.admitted_out = admitted_out;
+  p.used_out = used_out;
+  p.err = c->err;
+  const int blocks = (int)(((int64_t)p.n * 32 + 255) / 256);
+  pf::baseline_kernel<<<blocks, 256, 0, S(stream)>>>(p);
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
 }
 
 pf_status pf_get_device_error(pf_ctx* c, int32_t* code, int32_t* index, void* stream) {

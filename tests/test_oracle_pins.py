@@ -381,3 +381,41 @@ def test_shared_distribution_is_concatenation_of_shards():
     win = rows[8:16].reshape(-1)
     exp = [O.predict(win, int(x), 40, 0x12345678) for x in lt]
     assert list(out["pred_run"]) == exp
+
+
+# ------------------------------------------------------------------ baseline policies
+def test_aggressive_spec_examples():
+    # capacity 100, watermark 90 %, consumed 80: input 10 admitted
+    # (90 ≤ 90), a further input 1 rejected (91 > 90).
+    assert O.admit_aggressive([80], [0], [10], 100, 9000) == (1, 90)
+    assert O.admit_aggressive([80], [0], [10, 1], 100, 9000) == (1, 90)
+    assert O.admit_aggressive([70], [10], [10, 1], 100, 9000) == (1, 90)  # consumed = l_p + l_t
+
+
+def test_conservative_spec_examples():
+    # capacity 100, candidates (10, max_new 50): one fits without
+    # overcommit (60 ≤ 100), the second does not (120 > 100); with 150 % both fit.
+    assert O.admit_conservative([], [10, 10], 50, 100, 10000) == (1, 60)
+    assert O.admit_conservative([], [10, 10], 50, 100, 15000) == (2, 120)
+    assert O.admit_conservative([5], [10], 50, 100, 10000) == (0, 55)  # running budget l_p + max_new
+
+
+def test_baseline_policies_brute_force():
+    rng = random.Random(11)
+    for _ in range(400):
+        k, q = rng.randint(0, 6), rng.randint(0, 6)
+        mx = rng.randint(1, 40)
+        lp = [rng.randint(0, 30) for _ in range(k)]
+        lt = [rng.randint(0, mx - 1) for _ in range(k)]
+        ql = [rng.randint(0, 30) for _ in range(q)]
+        cap = rng.randint(0, 300)
+        wm = rng.choice([9000, 9500, 9900, 10000])
+        p = 0
+        while p < q and 10000 * (sum(lp) + sum(lt) + sum(ql[:p + 1])) <= wm * cap:
+            p += 1
+        assert O.admit_aggressive(lp, lt, ql, cap, wm) == (p, sum(lp) + sum(lt) + sum(ql[:p]))
+        oc = rng.choice([10000, 12500, 15000])
+        p = 0
+        while p < q and 10000 * (sum(lp) + k * mx + sum(ql[:p + 1]) + (p + 1) * mx) <= oc * cap:
+            p += 1
+        assert O.admit_conservative(lp, ql, mx, cap, oc) == (p, sum(lp) + k * mx + sum(ql[:p]) + p * mx)
