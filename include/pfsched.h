@@ -110,7 +110,8 @@ typedef struct {
   int32_t member_base;       /*   g·members_per_group + member_base + (l − group_off[g])      */
   int32_t mode;            /* PF_MODE_SAMPLE | PF_MODE_QUANTILE                               */
   uint32_t quantile_u;     /* u in quantile mode (0x80000000 = median rank)                   */
-  int32_t repetitions;     /* R >= 1 (C-9)                                                     */
+  int32_t repetitions;     /* R >= 1 (C-9); 0 = adaptive R = max(1, ⌈64/k⌉) per instance
+                              (k = running batch size; SPEC.md:161 reading of PAPER.md:295) */
   int32_t reserved_bp;     /* reserved ratio in basis points, 0..9999 (C-13)                   */
   uint64_t seed;           /* sampling-mode seed (C-8)                                         */
   int32_t rank, nranks;    /* shared mode: this rank owns shards {s in 0..7 : s % nranks == rank} */

@@ -373,7 +373,9 @@ static int32_t admit_instance(const orc_ctx* c, const orc_admit_args* A, int32_t
   // Alg.1 line 1: the distribution P(l) is the window L_h (Eq.(eq:5)).
   std::vector<int32_t> window = window_of(c, A->dist_of[i]);
   std::sort(window.begin(), window.end());
-  const int32_t R = A->repetitions;
+  // R > 0: fixed repetitions; R = 0: SPEC.md:161's reading of "repeated several times
+  // when the size of the running batch is low": R = max(1, ⌈64/k⌉), k = 0 → 64.
+  const int32_t R = A->repetitions > 0 ? A->repetitions : (k > 0 ? std::max(1, (64 + k - 1) / k) : 64);
   const uint64_t key = orc_instance_key(A->seed, A->tick, A->inst_id[i]);
   auto predict = [&](int32_t l_t, int32_t slot) -> int32_t {
     if (A->mode == 1) return predict_on_sorted(window, l_t, max_new, A->quantile_u);

@@ -363,10 +363,12 @@ admit_kernel(AdmitParams p) {
   const bool want_pred = (p.pred_run_out != nullptr) || (p.pred_q_out != nullptr);
   int my_bad = 0;
   // u of request slot e (C-8/C-9): one lowbias32 in the common case (sampling, R = 1)
-  const bool draw_fast = (p.mode == 0) && (p.R == 1);
+  // R = 0: adaptive repetitions max(1, ⌈64/k⌉) (SPEC.md:161 reading of PAPER.md:295)
+  const int R = p.R > 0 ? p.R : (k > 0 ? ::max(1, (64 + k - 1) / k) : 64);
+  const bool draw_fast = (p.mode == 0) && (R == 1);
   auto draw = [&](int e) -> uint32_t {
     uint32_t u = lowbias32(key_fold ^ ((uint32_t)e * 0x9E3779B9U));
-    if (!draw_fast) u = (p.mode != 0) ? p.quantile_u : draw_u(key_fold, e, p.R);
+    if (!draw_fast) u = (p.mode != 0) ? p.quantile_u : draw_u(key_fold, e, R);
     return u;
   };
   // l̂ → r, a; bin; push; (A, N) into the running or queue bins

@@ -150,7 +150,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   if (C.max_input_len < 0) return fail(PF_EINVAL, "max_input_len must be >= 0");
   if (C.max_entries < 1 || C.max_entries > 4096)
     return fail(PF_ERANGE, "max_entries must be in [1, 4096]");
-  if (C.repetitions < 1) return fail(PF_EINVAL, "repetitions must be >= 1");
+  if (C.repetitions < 0) return fail(PF_EINVAL, "repetitions must be >= 0 (0 = adaptive)");
   if (C.reserved_bp < 0 || C.reserved_bp > 9999) return fail(PF_EINVAL, "reserved_bp must be in [0, 9999]");
   if (C.mode != PF_MODE_SAMPLE && C.mode != PF_MODE_QUANTILE) return fail(PF_EINVAL, "bad mode");
   if ((int64_t)C.max_entries * ((int64_t)C.max_input_len + 2LL * C.max_len) >= (1LL << 31))

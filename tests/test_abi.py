@@ -47,7 +47,7 @@ def _cfg(**kw):
 
 @pytest.mark.parametrize("kw,status", [
     (dict(n_instances=0), -1), (dict(window=0), -1), (dict(max_len=0), -2), (dict(max_len=40000), -2),
-    (dict(max_entries=5000), -2), (dict(repetitions=0), -1), (dict(reserved_bp=10000), -1),
+    (dict(max_entries=5000), -2), (dict(repetitions=-1), -1), (dict(reserved_bp=10000), -1),
     (dict(mode=7), -1), (dict(max_input_len=10**7, max_entries=4096), -2),
     (dict(n_groups=2, window=100), -1), (dict(n_groups=2, window=96), -1),
     (dict(n_groups=2, window=96, group_off=1234, nranks=3), -1),

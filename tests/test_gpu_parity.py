@@ -49,6 +49,7 @@ CASES = [
     (3, 40, 0, 300, 1), (3, 16, 1, 0, 2),
     (4, 24, 0, 500, 1), (4, 12, 1, 1000, 3),
     (5, 128, 0, 500, 1), (5, 64, 1, 300, 2),
+    (5, 64, 0, 500, 0), (2, 16, 0, 0, 0),  # R = 0: adaptive repetitions max(1, ceil(64/k))
 ]
 
 

@@ -419,3 +419,16 @@ def test_baseline_policies_brute_force():
         while p < q and 10000 * (sum(lp) + k * mx + sum(ql[:p + 1]) + (p + 1) * mx) <= oc * cap:
             p += 1
         assert O.admit_conservative(lp, ql, mx, cap, oc) == (p, sum(lp) + k * mx + sum(ql[:p]) + p * mx)
+
+
+def test_adaptive_repetitions_rule():
+    # R = max(1, ceil(64 / k)); prediction = max of the R samples. With a
+    # 2-request batch R = 32: each prediction equals the quantile at the max of 32 draws.
+    win = np.arange(1, 101, dtype=np.int32)
+    orc = O.Oracle(1, 100, 200, 1, win[None, :])
+    out = orc.admit(dist_of=[0], inst_id=[5], run_off=[0, 2], input_len=[3, 4], generated=[0, 50],
+                    max_new=[200], mode=0, repetitions=0, seed=9, tick=2, want_pred=True)
+    K = O.instance_key(9, 2, 5)
+    for s, l_t in enumerate((0, 50)):
+        umax = max(O.draw(K, s, 32, rep) for rep in range(32))
+        assert out["pred_run"][s] == O.predict(win, l_t, 200, umax)
