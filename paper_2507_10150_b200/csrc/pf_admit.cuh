@@ -290,11 +290,14 @@ admit_kernel(AdmitParams p) {
   const int w = p.w;
   const uint16_t* gC = nullptr;
   const uint16_t* gS = nullptr;
+  int goffC = 0, goffS = 0;  // element offsets of the group's rows (32-bit index math)
   int64_t gid;
   if (LOOK == LOOK_GROUP) {
     const int g = p.dist_of[i];
-    gC = p.gC + (int64_t)g * p.c_stride;
-    gS = p.gS + (int64_t)g * p.s_stride;
+    goffC = g * p.c_stride;
+    goffS = g * p.s_stride;
+    gC = p.gC + goffC;
+    gS = p.gS + goffS;
     gid = (int64_t)g * p.members_per_group + p.member_base + (i - p.group_off[g]);
   } else {
     gid = p.instance_base + i;
@@ -442,8 +445,8 @@ admit_kernel(AdmitParams p) {
       my_bad |= (e < k) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
                            ((unsigned)lt[c] >= (unsigned)max_new));
       lt[c] = ::min(::max(lt[c], 0), max_new - 1);  // keep lookups in range; outputs dropped if bad
-      u[c] = draw(e);
-      if (LOOK == LOOK_GROUP) bq[c] = __ldg(gC + lt[c]);
+      u[c] = lowbias32(key_fold ^ ((uint32_t)e * 0x9E3779B9U));  // C-8, R = 1
+      if (LOOK == LOOK_GROUP) bq[c] = __ldg(p.gC + (goffC + lt[c]));
       else if (LOOK == LOOK_HIST) bq[c] = table[lt[c]];
       else {  // #{S ≤ l_t}: first S > l_t inside the coarse bucket of l_t
         const int cb = lt[c] >> csh;
@@ -455,12 +458,16 @@ admit_kernel(AdmitParams p) {
         bq[c] = lo;
       }
     }
+    if (!draw_fast) {  // quantile mode or R ≠ 1: one uniform branch per chunk
+#pragma unroll
+      for (int c = 0; c < 4; ++c) u[c] = draw(e0 + c * TT);
+    }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int n_gt = w - bq[c];
       const int x = bq[c] + (int)__umulhi(u[c], (uint32_t)n_gt);
       if (LOOK == LOOK_GROUP) {
-        lh[c] = n_gt ? (int)__ldg(gS + x) : max_new;
+        lh[c] = n_gt ? (int)__ldg(p.gS + (goffS + x)) : max_new;
       } else if (LOOK == LOOK_SORTED) {
         lh[c] = n_gt ? table[x] : max_new;
       } else {
@@ -495,7 +502,7 @@ admit_kernel(AdmitParams p) {
       my_bad |= (j < q) & ((unsigned)lp[c] > (unsigned)p.max_input_len);
       const int x = (int)__umulhi(draw(k + j), (uint32_t)w);
       if (LOOK == LOOK_GROUP) {
-        lh[c] = __ldg(gS + x);
+        lh[c] = __ldg(p.gS + (goffS + x));
       } else if (LOOK == LOOK_SORTED) {
         lh[c] = table[x];
       } else {
