@@ -70,7 +70,7 @@ struct AdmitParams {
   int members_per_group, member_base;
   int team_smem;       // bytes of shared memory per team
   int ent_cap;         // request slots per team (>= max_entries)
-  const uint16_t* bintab;  // [Lmax+1]: r -> bin
+  int bin_shift;            // s of the r -> bin map (bin_of)
   const uint32_t* edges;   // [n_bins]: lo | hi << 16 (0 = no r maps to the bin)
   // history tables
   const int32_t* sorted;     // LOOK_SORTED [n × w]
@@ -100,6 +100,18 @@ struct AdmitParams {
   const int32_t* lhat_run;   // [run_off[n]]
   const int32_t* lhat_q;     // [q_off[n]]
 };
+
+// r -> bin (r ≥ 1), the log-linear map of DESIGN.md §5 computed in registers: f(r) = r − 1
+// for r ≤ 2^(KO+1) (exact bins), else 2^KO·sh + (r >> sh) with sh = min(⌊log2 r⌋ − KO, s)
+// (2^KO bins per octave, then width 2^s); bins are stored descending, b = NB − 1 − f(r).
+// The host builds the per-bin edges from the same map (pfsched.cu bin_f).
+template <int NB>
+__device__ __forceinline__ int bin_of(int r, int s) {
+  constexpr int KO = (PF_BPT == 2) ? 2 : (PF_BPT == 4) ? 3 : 4;
+  const int sh = ::min(31 - KO - __clz(r), s);
+  const int f = r <= (2 << KO) ? r - 1 : (sh << KO) + (r >> sh);
+  return NB - 1 - f;
+}
 
 // #{x in S[0..w) : x <= v} for ascending S (upper_bound).
 __device__ __forceinline__ int upper_bound_smem(const int32_t* S, int w, int v) {
@@ -376,15 +388,11 @@ admit_kernel(AdmitParams p) {
   };
   // l̂ → r, a; bin; push; (A, N) into the running or queue bins
   const bool override_lhat = p.lhat_run != nullptr;
+  // (prediction outputs are stored by the callers, in one uniform branch per chunk)
   auto finish = [&](int e, int l_hat, int l_t, int l_p, bool run) {
-    if (!override_lhat) l_hat = ::min(l_hat, max_new);  // C-6
-    if (want_pred) {
-      int32_t* pout = run ? p.pred_run_out : p.pred_q_out;
-      if (pout) pout[run ? r0 + e : q0 - k + e] = l_hat;
-    }
     const int r = l_hat - l_t;  // ≥ 1 (C-4)
     const int a = l_p + l_t;
-    const int b = __ldg(p.bintab + r);
+    const int b = bin_of<NB>(r, p.bin_shift);
     if (PACK) {
       rb[e] = (uint32_t)r | ((uint32_t)a << 13);
     } else {
@@ -414,6 +422,7 @@ admit_kernel(AdmitParams p) {
       const bool bad = (unsigned)l_p > (unsigned)p.max_input_len || l_t < 0 || l_hat <= l_t ||
                        l_hat > p.max_len;
       my_bad |= bad;
+      if (!bad && want_pred && p.pred_run_out) p.pred_run_out[r0 + e] = l_hat;
       if (!bad) finish(e, l_hat, l_t, l_p, true);
     }
 #pragma unroll 1
@@ -421,6 +430,7 @@ admit_kernel(AdmitParams p) {
       const int l_p = __ldg(p.q_input_len + q0 + j), l_hat = __ldg(p.lhat_q + q0 + j);
       const bool bad = (unsigned)l_p > (unsigned)p.max_input_len || l_hat < 1 || l_hat > p.max_len;
       my_bad |= bad;
+      if (!bad && want_pred && p.pred_q_out) p.pred_q_out[q0 + j] = l_hat;
       if (!bad) finish(k + j, l_hat, 0, l_p, false);
     }
   } else {
@@ -480,6 +490,12 @@ admit_kernel(AdmitParams p) {
         }
         lh[c] = n_gt ? lo : max_new;
       }
+      lh[c] = ::min(lh[c], max_new);  // C-6
+    }
+    if (want_pred && p.pred_run_out) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (e0 + c * TT < k) p.pred_run_out[r0 + e0 + c * TT] = lh[c];
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -493,6 +509,7 @@ admit_kernel(AdmitParams p) {
 #pragma unroll 1
   for (int j0 = tid; j0 < q; j0 += 4 * TT) {
     int lp[4], lh[4];
+    uint32_t u[4];
     const int32_t* qpp = qp_base + j0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) lp[c] = (j0 + c * TT < q) ? __ldg(qpp + c * TT) : 0;
@@ -500,7 +517,15 @@ admit_kernel(AdmitParams p) {
     for (int c = 0; c < 4; ++c) {
       const int j = j0 + c * TT;
       my_bad |= (j < q) & ((unsigned)lp[c] > (unsigned)p.max_input_len);
-      const int x = (int)__umulhi(draw(k + j), (uint32_t)w);
+      u[c] = lowbias32(key_fold ^ ((uint32_t)(k + j) * 0x9E3779B9U));  // C-8, R = 1
+    }
+    if (!draw_fast) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) u[c] = draw(k + j0 + c * TT);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int x = (int)__umulhi(u[c], (uint32_t)w);
       if (LOOK == LOOK_GROUP) {
         lh[c] = __ldg(p.gS + (goffS + x));
       } else if (LOOK == LOOK_SORTED) {
@@ -515,6 +540,12 @@ admit_kernel(AdmitParams p) {
         }
         lh[c] = lo;
       }
+      lh[c] = ::min(lh[c], max_new);  // C-6
+    }
+    if (want_pred && p.pred_q_out) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (j0 + c * TT < q) p.pred_q_out[q0 + j0 + c * TT] = lh[c];
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -838,7 +869,7 @@ admit_kernel(AdmitParams p) {
     }
     T.sync();
     for (int jx = tid; jx < ph; jx += TT) {
-      const int b = PACK ? (int)__ldg(p.bintab + ent_r(k + jx)) : (int)(rb[k + jx] >> 16);
+      const int b = PACK ? bin_of<NB>(ent_r(k + jx), p.bin_shift) : (int)(rb[k + jx] >> 16);
       const int a = ent_a(k + jx);
       if (PACK) {
         atomicAdd(&binQ[b], ((uint32_t)a << 9) | 1u);

@@ -88,7 +88,6 @@ struct pf_ctx {
   int32_t* group_off = nullptr;
   int* err = nullptr;  // [2] code, index
   int* scratch = nullptr;
-  uint16_t* bintab = nullptr;  // [Lmax+1] r -> bin
   uint32_t* edges = nullptr;   // [n_bins] lo | hi << 16
   int pack;
   int variant;
@@ -103,7 +102,7 @@ void free_ctx(pf_ctx* c) {
   if (!c) return;
   for (void* p : {(void*)c->ring, (void*)c->head, (void*)c->sorted, (void*)c->hist,
                   (void*)c->xbuf, (void*)c->gC, (void*)c->gS, (void*)c->dist_of,
-                  (void*)c->group_off, (void*)c->err, (void*)c->scratch, (void*)c->bintab,
+                  (void*)c->group_off, (void*)c->err, (void*)c->scratch,
                   (void*)c->edges})
     if (p) cudaFree(p);
   delete c;
@@ -256,18 +255,14 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   c->n_bins = 32 * PF_BPT * V.TW;
   c->bin_shift = 1;
   while (bin_f(C.max_len, c->bin_shift) > c->n_bins - 1) ++c->bin_shift;
-  {  // r -> bin table and per-bin r ranges
-    std::vector<uint16_t> tab(C.max_len + 1, 0);
+  {  // per-bin r ranges of the r -> bin map (the kernel computes the map: bin_of)
     std::vector<uint32_t> ed(c->n_bins, 0);
     for (int r = 1; r <= C.max_len; ++r) {
       const int b = c->n_bins - 1 - bin_f(r, c->bin_shift);
-      tab[r] = (uint16_t)b;
       const uint32_t lo = ed[b] ? (ed[b] & 0xFFFF) : (uint32_t)r;
       ed[b] = lo | ((uint32_t)r << 16);
     }
-    PF_CUDA_C(cudaMalloc(&c->bintab, tab.size() * 2 + 16));
     PF_CUDA_C(cudaMalloc(&c->edges, ed.size() * 4 + 16));
-    PF_CUDA_C(cudaMemcpy(c->bintab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice));
     PF_CUDA_C(cudaMemcpy(c->edges, ed.data(), ed.size() * 4, cudaMemcpyHostToDevice));
   }
   // PACK: per-bin (A, N) fit one 32-bit word (A << 9 | N: every bin sum < 2^23, count
@@ -367,7 +362,7 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.instance_base = C.instance_base;
   p.members_per_group = C.members_per_group;
   p.member_base = C.member_base;
-  p.bintab = c->bintab;
+  p.bin_shift = c->bin_shift;
   p.edges = c->edges;
   p.team_smem = c->team_smem;
   p.ent_cap = c->ent_cap;
