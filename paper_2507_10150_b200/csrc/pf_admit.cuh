@@ -45,6 +45,10 @@
 #ifndef PF_MINMAX
 #define PF_MINMAX 1
 #endif
+// Prefetch of the instance's input streams at kernel entry: 1 = L1, 2 = L2, 0 = off.
+#ifndef PF_PREFETCH
+#define PF_PREFETCH 0
+#endif
 template <int TW>
 struct MinMax {
   static constexpr bool on = PF_MINMAX && TW > 1;
@@ -111,6 +115,15 @@ __device__ __forceinline__ int bin_of(int r, int s) {
   const int sh = ::min(31 - KO - __clz(r), s);
   const int f = r <= (2 << KO) ? r - 1 : (sh << KO) + (r >> sh);
   return NB - 1 - f;
+}
+
+// L1 prefetch of the 128-byte lines covering x[0..n), one line per thread per pass.
+__device__ __forceinline__ void prefetch_lines(const int32_t* x, int n, int tid, int tt) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(x) & ~(uintptr_t)127;
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(x + n);
+  for (uintptr_t a = a0 + (uintptr_t)tid * 128; a < a1; a += (uintptr_t)tt * 128)
+    if (PF_PREFETCH == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+    else asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
 }
 
 // #{x in S[0..w) : x <= v} for ascending S (upper_bound).
@@ -232,7 +245,10 @@ struct Eval {
 //   table            S[w] (LOOK_SORTED) | C[Lmax+1] (LOOK_HIST)
 // CTA prefix: edges[NB] u32 shared by the teams.
 template <int TW, int LOOK, bool PACK>
-__global__ void __launch_bounds__((TW == 1 ? 4 : 1) * TW * 32, (TW == 1 ? 8 : 2))
+#ifndef PF_MIN_CTAS
+#define PF_MIN_CTAS 8
+#endif
+__global__ void __launch_bounds__((TW == 1 ? 4 : 1) * TW * 32, (TW == 1 ? PF_MIN_CTAS : 2))
 admit_kernel(AdmitParams p) {
   constexpr int TT = TW * 32;
   constexpr int TEAMS = (TW == 1) ? 4 : 1;
@@ -276,6 +292,13 @@ admit_kernel(AdmitParams p) {
   const int k = r1 - r0, q = q1 - q0, n_ent = k + q;
   const int max_new = p.max_new ? p.max_new[i] : p.max_len;
   const int cap = estimate_only ? 0 : p.capacity[i];
+  if (PF_PREFETCH && k > 0 && q >= 0 && n_ent <= p.max_entries && p.lhat_run == nullptr) {
+    // put the instance's input streams in flight now (L1 prefetch, one 128-byte line per
+    // thread): their HBM latency then overlaps the scalar chain and the shared-memory setup
+    prefetch_lines(p.input_len + r0, k, tid, TT);
+    prefetch_lines(p.generated + r0, k, tid, TT);
+    if (q > 0) prefetch_lines(p.q_input_len + q0, q, tid, TT);
+  }
   int bad = 0;
   if (k < 0 || q < 0 || n_ent > p.max_entries) bad = PF_BAD_OFFSETS;
   else if (max_new < 1 || max_new > p.max_len) bad = PF_BAD_MAX_NEW;
@@ -434,27 +457,33 @@ admit_kernel(AdmitParams p) {
       if (!bad) finish(k + j, l_hat, 0, l_p, false);
     }
   } else {
-  const int32_t* lp_base = p.input_len + r0;
-  const int32_t* lt_base = p.generated + r0;
+  // All k + q entries in one loop (slot e: running e < k, queued e ≥ k with l_t = 0,
+  // C-16), 4 per thread per chunk with the chunk's loads issued together. For a queued
+  // entry C[0] = 0 (history ≥ 1), so the running formula gives P(l) unchanged.
+  const int32_t* lpR = p.input_len + r0;
+  const int32_t* ltR = p.generated + r0;
+  const int32_t* lpQ = p.q_input_len + (q0 - k);  // indexed by slot e ≥ k
+  int32_t* poR = p.pred_run_out ? p.pred_run_out + r0 : nullptr;
+  int32_t* poQ = p.pred_q_out ? p.pred_q_out + (q0 - k) : nullptr;
 #pragma unroll 1
-  for (int e0 = tid; e0 < k; e0 += 4 * TT) {
+  for (int e0 = tid; e0 < n_ent; e0 += 4 * TT) {
     int lp[4], lt[4], bq[4], lh[4];
     uint32_t u[4];
-    const int32_t* lpp = lp_base + e0;  // + c·TT: immediate offsets
-    const int32_t* ltp = lt_base + e0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const bool in = e0 + c * TT < k;
-      lp[c] = in ? __ldg(lpp + c * TT) : 0;
-      lt[c] = in ? __ldg(ltp + c * TT) : 0;
+      const int e = e0 + c * TT;
+      const bool run = e < k;
+      lp[c] = (e < n_ent) ? __ldg((run ? lpR : lpQ) + e) : 0;
+      lt[c] = run ? __ldg(ltR + e) : 0;
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int e = e0 + c * TT;
       // l_p ∉ [0, max_input_len] or l_t ∉ [0, max_new) (unsigned compares catch < 0)
-      my_bad |= (e < k) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
-                           ((unsigned)lt[c] >= (unsigned)max_new));
-      lt[c] = ::min(::max(lt[c], 0), max_new - 1);  // keep lookups in range; outputs dropped if bad
+      my_bad |= (e < n_ent) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
+                               ((unsigned)lt[c] >= (unsigned)max_new));
+      // keep lookups in range (outputs are dropped when bad): unsigned min maps l_t < 0 too
+      lt[c] = (int)::min((unsigned)lt[c], (unsigned)(max_new - 1));
       u[c] = lowbias32(key_fold ^ ((uint32_t)e * 0x9E3779B9U));  // C-8, R = 1
       if (LOOK == LOOK_GROUP) bq[c] = __ldg(p.gC + (goffC + lt[c]));
       else if (LOOK == LOOK_HIST) bq[c] = table[lt[c]];
@@ -492,65 +521,18 @@ admit_kernel(AdmitParams p) {
       }
       lh[c] = ::min(lh[c], max_new);  // C-6
     }
-    if (want_pred && p.pred_run_out) {
+    if (want_pred) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (e0 + c * TT < k) p.pred_run_out[r0 + e0 + c * TT] = lh[c];
+      for (int c = 0; c < 4; ++c) {
+        const int e = e0 + c * TT;
+        int32_t* po = e < k ? poR : poQ;
+        if (e < n_ent && po) po[e] = lh[c];
+      }
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int e = e0 + c * TT;
-      if (e < k) finish(e, lh[c], lt[c], lp[c], true);
-    }
-  }
-  // queued requests j ∈ [0, q), slot e = k + j: l̂ from P(l) — every history value
-  // exceeds l_t = 0 (C-16), so base = 0 and n_gt = w: one lookup
-  const int32_t* qp_base = p.q_input_len + q0;
-#pragma unroll 1
-  for (int j0 = tid; j0 < q; j0 += 4 * TT) {
-    int lp[4], lh[4];
-    uint32_t u[4];
-    const int32_t* qpp = qp_base + j0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) lp[c] = (j0 + c * TT < q) ? __ldg(qpp + c * TT) : 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = j0 + c * TT;
-      my_bad |= (j < q) & ((unsigned)lp[c] > (unsigned)p.max_input_len);
-      u[c] = lowbias32(key_fold ^ ((uint32_t)(k + j) * 0x9E3779B9U));  // C-8, R = 1
-    }
-    if (!draw_fast) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) u[c] = draw(k + j0 + c * TT);
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int x = (int)__umulhi(u[c], (uint32_t)w);
-      if (LOOK == LOOK_GROUP) {
-        lh[c] = __ldg(p.gS + (goffS + x));
-      } else if (LOOK == LOOK_SORTED) {
-        lh[c] = table[x];
-      } else {
-        int lo = 1, len = p.max_len;  // smallest L with C[L] > x
-        while (len > 0) {
-          const int half = len >> 1;
-          const bool right = table[lo + half] <= x;
-          lo = right ? lo + half + 1 : lo;
-          len = right ? len - half - 1 : half;
-        }
-        lh[c] = lo;
-      }
-      lh[c] = ::min(lh[c], max_new);  // C-6
-    }
-    if (want_pred && p.pred_q_out) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (j0 + c * TT < q) p.pred_q_out[q0 + j0 + c * TT] = lh[c];
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = j0 + c * TT;
-      if (j < q) finish(k + j, lh[c], 0, lp[c], false);
+      if (e < n_ent) finish(e, lh[c], lt[c], lp[c], e < k);
     }
   }
   }  // !override_lhat
