@@ -20,6 +20,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "pf_oracle.cpp")
+_SRCS = [_SRC, os.path.join(_HERE, "pf_sim_oracle.cpp")]
 _LIB_PATH = os.path.join(_HERE, "liborc.so")
 _lib = None
 
@@ -32,9 +33,11 @@ ORC_E_INPUT_LEN, ORC_E_GENERATED, ORC_E_CAPACITY = 4, 5, 6
 
 def build_oracle(force: bool = False) -> str:
     """Compile liborc.so with plain g++ (-O2, no SIMD intrinsics)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+    stale = not os.path.exists(_LIB_PATH) or any(
+        os.path.getmtime(_LIB_PATH) < os.path.getmtime(f) for f in _SRCS)
+    if force or stale:
         subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-pthread",
-                               _SRC, "-o", _LIB_PATH])
+                               *_SRCS, "-o", _LIB_PATH])
     return _LIB_PATH
 
 
@@ -53,6 +56,25 @@ class _AdmitArgs(ctypes.Structure):
         ("pred_run_out", I32P), ("pred_q_out", I32P),
         ("first_error", I32P), ("first_error_inst", I32P),
     ]
+
+
+class _SimArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_inst", ctypes.c_int32),
+        ("req_off", I32P), ("req_input", I32P), ("req_output", I32P),
+        ("max_new", I32P), ("capacity", I32P),
+        ("policy", ctypes.c_int32), ("param_bp", ctypes.c_int32),
+        ("window", ctypes.c_int32), ("max_len", ctypes.c_int32), ("init_history", I32P),
+        ("max_entries", ctypes.c_int32),
+        ("mode", ctypes.c_int32), ("quantile_u", ctypes.c_uint32), ("repetitions", ctypes.c_int32),
+        ("seed", ctypes.c_uint64), ("instance_base", ctypes.c_int64), ("iterations", ctypes.c_int32),
+        ("metrics_out", I64P), ("generated_out", I32P), ("evictions_out", I32P),
+    ]
+
+
+SIM_PAST_FUTURE, SIM_OPTIMUM, SIM_AGGRESSIVE, SIM_CONSERVATIVE = 0, 1, 2, 3
+SIM_METRICS = ("iterations", "decode_steps", "evictions", "finished", "consumed_sum",
+               "future_sum", "samples", "future_max", "forced", "admissions")
 
 
 def lib():
@@ -100,6 +122,10 @@ def lib():
         L.orc_admit_conservative.argtypes = [ctypes.c_int32, I32P, ctypes.c_int32, I32P, ctypes.c_int32,
                                              ctypes.c_int64, ctypes.c_int32, I64P]
         assert L.orc_sizeof_admit_args() == ctypes.sizeof(_AdmitArgs), "oracle ABI struct mismatch"
+        L.orc_sim_run.restype = None
+        L.orc_sim_run.argtypes = [ctypes.POINTER(_SimArgs), ctypes.c_int32]
+        L.orc_sizeof_sim_args.restype = ctypes.c_int32
+        assert L.orc_sizeof_sim_args() == ctypes.sizeof(_SimArgs), "oracle sim ABI struct mismatch"
         _lib = L
     return _lib
 
@@ -275,3 +301,28 @@ class Oracle:
             if pred_q is not None:
                 out["pred_q"] = pred_q[:n_q]
         return out
+
+
+# ---------------------------------------------------------------- simulator (NEXT-2)
+def sim_run(*, req_off, req_input, req_output, max_new, capacity, policy, param_bp, window,
+            max_len, max_entries, iterations, init_history=None, mode=0, quantile_u=0x80000000,
+            repetitions=1, seed=0, instance_base=0, n_threads=None):
+    """Continuous-batching simulation of every instance for ``iterations`` iterations
+    (pf_sim_oracle.cpp, readings S-1..S-9). Returns (metrics [n × 10] int64 with
+    columns SIM_METRICS, generated per request, evictions per request)."""
+    ro, ri, rq = _i32(req_off), _i32(req_input), _i32(req_output)
+    ih = None if init_history is None else _i32(init_history).reshape(-1)
+    mn, cap = _i32(max_new), _i32(capacity)
+    n = len(mn)
+    n_req = int(ro[-1])
+    met = np.zeros((n, len(SIM_METRICS)), np.int64)
+    gen = np.zeros(max(n_req, 1), np.int32)
+    ev = np.zeros(max(n_req, 1), np.int32)
+    if n_req == 0:
+        ri = rq = np.zeros(1, np.int32)
+    args = _SimArgs(n, _p32(ro), _p32(ri), _p32(rq), _p32(mn), _p32(cap), policy, param_bp, window,
+                    max_len, _p32(ih), max_entries, mode, quantile_u & 0xFFFFFFFF, repetitions,
+                    seed & 0xFFFFFFFFFFFFFFFF, instance_base, iterations,
+                    met.ctypes.data_as(I64P), _p32(gen), _p32(ev))
+    lib().orc_sim_run(ctypes.byref(args), n_threads or os.cpu_count() or 1)
+    return met, gen[:n_req], ev[:n_req]
