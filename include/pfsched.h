@@ -214,6 +214,79 @@ pf_status pf_clear_device_error(pf_ctx* ctx, void* stream);
  * (checkpoint / test hook; same layout as init_history). Enqueued on `stream`. */
 pf_status pf_export_history(pf_ctx* ctx, int32_t* rows_out, void* stream);
 
+/* ------------------------------------------------------------------------------------
+ * Batched continuous-batching simulator: the serving loop the
+ * paper's Table 1 measures ("Decoding Steps", "Current Consumed
+ * Memory", "Future Required Memory", "Evicted Reqs"), one independent simulation per
+ * instance, all instances advanced together on the device with the admission calls
+ * above. Iteration semantics (readings S-1..S-9):
+ *   S-1 every request of an instance is queued at t = 0 in list order;
+ *   S-2 running requests with generated == true length finish; their lengths are
+ *       recorded into the instance's window;
+ *   S-3 admission over (running, the first min(|queue|, E − k) queued requests) by the
+ *       policy: PF_SIM_PAST_FUTURE = pf_admit (tick = iteration index, reserved ratio
+ *       param_bp); PF_SIM_OPTIMUM = pf_admit_override with the true lengths (the paper's
+ *       "Theoretical optimum"; reserved param_bp); PF_SIM_AGGRESSIVE /
+ *       PF_SIM_CONSERVATIVE = pf_admit_baseline (watermark / overcommit param_bp).
+ *       A queued request enters with l_p + generated (evicted requests recompute);
+ *   S-4 the admitted FIFO prefix joins the running list; an empty batch takes the queue
+ *       head regardless (progress, counted as "forced");
+ *   S-5 future-required sample: M* (Eq.(eq:1)-(eq:3)) of the running set with TRUE
+ *       remaining lengths;
+ *   S-6 while Σ(l_p + l_t) + k > M and k > 1: evict the most recently admitted request,
+ *       re-queue it at the FRONT with its generated tokens (LIFO);
+ *   S-7 decode: every running request gains one token;
+ *   S-8 consumed sample Σ(l_p + l_t);  S-9 done when queue and batch are empty.
+ * Metrics per instance (int64, PF_SIM_NMETRICS columns): iterations, decoding steps,
+ * evictions, finished requests, Σ consumed, Σ future, samples, max future, forced
+ * admissions, admissions. Averages / capacity give Table 1's percentages. */
+typedef struct pf_sim pf_sim;
+enum { PF_SIM_PAST_FUTURE = 0, PF_SIM_OPTIMUM = 1, PF_SIM_AGGRESSIVE = 2,
+       PF_SIM_CONSERVATIVE = 3 };
+#define PF_SIM_NMETRICS 10
+
+typedef struct {
+  int32_t n_instances;    /* independent simulations (>= 1)                              */
+  int32_t window;         /* history window w of each instance (C-1)                      */
+  int32_t max_len;        /* Lmax >= every max_new (C-2 initial window value)             */
+  int32_t max_input_len;  /* bound on request input lengths                              */
+  int32_t max_entries;    /* E: running + admission window per instance, 1..4096          */
+  int32_t policy;         /* PF_SIM_*                                                     */
+  int32_t param_bp;       /* reserved bp (0..9999) | watermark / overcommit bp (>= 1)     */
+  int32_t mode;           /* past-future prediction: PF_MODE_SAMPLE | PF_MODE_QUANTILE    */
+  uint32_t quantile_u;
+  int32_t repetitions;    /* R (C-9), 0 = adaptive                                        */
+  uint64_t seed;
+  int64_t instance_base;  /* hash key of instance i = instance_base + i (C-8)              */
+} pf_sim_config;
+
+/* Create a simulator. Device arrays (copied; the caller keeps ownership):
+ *   req_off [n+1] (requests of instance i are [req_off[i], req_off[i+1]), list order),
+ *   req_input / req_output [req_off[n]] (l_p in [0, max_input_len], true output length
+ *   in [1, max_new[i]]), max_new [n] in [1, max_len], capacity [n] (M, tokens, with
+ *   l_p + L <= M for every request), init_history [n × window] nullable (oldest first;
+ *   NULL ⇒ Lmax, C-2). Host-validated (synchronises `stream`); PF_EINVAL on violation. */
+pf_status pf_sim_create(const pf_sim_config* cfg, const int32_t* req_off,
+                        const int32_t* req_input, const int32_t* req_output,
+                        const int32_t* max_new, const int32_t* capacity,
+                        const int32_t* init_history, void* stream, pf_sim** out);
+
+/* Advance every instance by `iterations` iterations (finished instances idle). Enqueued. */
+pf_status pf_sim_step(pf_sim* sim, int32_t iterations, void* stream);
+
+/* Number of finished instances (synchronises `stream`). */
+pf_status pf_sim_done(pf_sim* sim, int32_t* n_done, void* stream);
+
+/* Copy metrics [n × PF_SIM_NMETRICS] int64 and, if non-NULL, generated tokens and
+ * eviction counts per request [req_off[n]] to device buffers. Enqueued. */
+pf_status pf_sim_metrics(pf_sim* sim, int64_t* metrics_out, int32_t* generated_out,
+                         int32_t* evictions_out, void* stream);
+
+/* The simulator's library context (device error word, history export). */
+pf_ctx* pf_sim_context(pf_sim* sim);
+
+pf_status pf_sim_destroy(pf_sim* sim);
+
 /* Describes the last failing call on this thread ("" if none). */
 const char* pf_last_error(void);
 

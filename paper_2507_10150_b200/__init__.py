@@ -6,7 +6,9 @@ The computation lives in libpfsched.so (CUDA kernels behind the C-ABI declared i
 include/pfsched.h); ``binding`` is a ctypes marshalling layer with the same names.
 """
 from .binding import (PF_MODE_QUANTILE, PF_MODE_SAMPLE, PF_POLICY_AGGRESSIVE, PF_POLICY_CONSERVATIVE,
-                      PFError, Scheduler, load, LIB_PATH, SYMBOLS)
+                      PF_SIM_AGGRESSIVE, PF_SIM_CONSERVATIVE, PF_SIM_OPTIMUM, PF_SIM_PAST_FUTURE,
+                      SIM_METRICS, PFError, Scheduler, Simulator, load, LIB_PATH, SYMBOLS)
 
-__all__ = ["Scheduler", "PFError", "load", "LIB_PATH", "SYMBOLS", "PF_MODE_SAMPLE",
-           "PF_MODE_QUANTILE", "PF_POLICY_AGGRESSIVE", "PF_POLICY_CONSERVATIVE"]
+__all__ = ["Scheduler", "Simulator", "PFError", "load", "LIB_PATH", "SYMBOLS", "PF_MODE_SAMPLE",
+           "PF_MODE_QUANTILE", "PF_POLICY_AGGRESSIVE", "PF_POLICY_CONSERVATIVE", "PF_SIM_PAST_FUTURE",
+           "PF_SIM_OPTIMUM", "PF_SIM_AGGRESSIVE", "PF_SIM_CONSERVATIVE", "SIM_METRICS"]

@@ -35,10 +35,25 @@ class PFConfig(ctypes.Structure):
     ]
 
 
+class PFSimConfig(ctypes.Structure):
+    _fields_ = [
+        ("n_instances", _i32), ("window", _i32), ("max_len", _i32), ("max_input_len", _i32),
+        ("max_entries", _i32), ("policy", _i32), ("param_bp", _i32), ("mode", _i32),
+        ("quantile_u", ctypes.c_uint32), ("repetitions", _i32), ("seed", ctypes.c_uint64),
+        ("instance_base", ctypes.c_int64),
+    ]
+
+
+PF_SIM_PAST_FUTURE, PF_SIM_OPTIMUM, PF_SIM_AGGRESSIVE, PF_SIM_CONSERVATIVE = 0, 1, 2, 3
+SIM_METRICS = ("iterations", "decode_steps", "evictions", "finished", "consumed_sum",
+               "future_sum", "samples", "future_max", "forced", "admissions")
+
 _lib = None
 SYMBOLS = ("pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer", "pf_commit_history",
            "pf_estimate_peak", "pf_admit", "pf_admit_override", "pf_admit_baseline", "pf_get_device_error",
-           "pf_clear_device_error", "pf_export_history", "pf_last_error", "pf_abi_version")
+           "pf_clear_device_error", "pf_export_history", "pf_last_error", "pf_abi_version",
+           "pf_sim_create", "pf_sim_step", "pf_sim_done", "pf_sim_metrics", "pf_sim_context",
+           "pf_sim_destroy")
 
 
 def load(path: str = LIB_PATH):
@@ -64,8 +79,15 @@ def load(path: str = LIB_PATH):
     L.pf_get_device_error.argtypes = [_vp, P(_i32), P(_i32), _vp]
     L.pf_clear_device_error.argtypes = [_vp, _vp]
     L.pf_export_history.argtypes = [_vp, _vp, _vp]
+    L.pf_sim_create.argtypes = [P(PFSimConfig)] + [_vp] * 7 + [P(_vp)]
+    L.pf_sim_step.argtypes = [_vp, _i32, _vp]
+    L.pf_sim_done.argtypes = [_vp, P(_i32), _vp]
+    L.pf_sim_metrics.argtypes = [_vp] * 5
+    L.pf_sim_context.argtypes = [_vp]
+    L.pf_sim_context.restype = _vp
+    L.pf_sim_destroy.argtypes = [_vp]
     for s in SYMBOLS:
-        if s not in ("pf_abi_version", "pf_last_error"):
+        if s not in ("pf_abi_version", "pf_last_error", "pf_sim_context"):
             getattr(L, s).restype = _i32
     assert L.pf_abi_version() == 1
     _lib = L
@@ -206,6 +228,73 @@ class Scheduler:
         out = torch.empty((self.rows, self.row_window), dtype=torch.int32, device="cuda")
         _check(load().pf_export_history(self._h, _ptr(out), _stream()), "pf_export_history")
         return out
+
+
+class Simulator:
+    """Batched continuous-batching simulator (pf_sim_*, NEXT-2): one serving simulation
+    per instance, advanced together on the device (readings S-1..S-9, include/pfsched.h)."""
+
+    def __init__(self, *, req_off, req_input, req_output, max_new, capacity, policy: int,
+                 param_bp: int, window: int, max_len: int, max_input_len: int, max_entries: int,
+                 init_history: Optional[torch.Tensor] = None, mode: int = PF_MODE_SAMPLE,
+                 quantile_u: int = 0x80000000, repetitions: int = 1, seed: int = 0,
+                 instance_base: int = 0):
+        L = load()
+        n = int(max_new.numel())
+        self.cfg = PFSimConfig(n, window, max_len, max_input_len, max_entries, policy, param_bp, mode,
+                               quantile_u & 0xFFFFFFFF, repetitions, seed & 0xFFFFFFFFFFFFFFFF,
+                               instance_base)
+        h = ctypes.c_void_p()
+        _check(L.pf_sim_create(ctypes.byref(self.cfg), _ptr(req_off), _ptr(req_input), _ptr(req_output),
+                               _ptr(max_new), _ptr(capacity), _ptr(init_history), _stream(),
+                               ctypes.byref(h)), "pf_sim_create")
+        self._h = h
+        self.n = n
+        self.n_req = int(req_input.numel())
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            load().pf_sim_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, iterations: int):
+        _check(load().pf_sim_step(self._h, iterations, _stream()), "pf_sim_step")
+
+    def n_done(self) -> int:
+        d = _i32()
+        _check(load().pf_sim_done(self._h, ctypes.byref(d), _stream()), "pf_sim_done")
+        return d.value
+
+    def run(self, chunk: int = 256, max_iterations: int = 1 << 30) -> int:
+        """Step until every instance is done; returns the iterations launched."""
+        it = 0
+        while it < max_iterations and self.n_done() < self.n:
+            c = min(chunk, max_iterations - it)
+            self.step(c)
+            it += c
+        return it
+
+    def metrics(self):
+        """-> (metrics [n, 10] int64, generated [N] int32, evictions [N] int32) on the device."""
+        m = torch.empty((self.n, len(SIM_METRICS)), dtype=torch.int64, device="cuda")
+        g = torch.empty(max(self.n_req, 1), dtype=torch.int32, device="cuda")
+        e = torch.empty_like(g)
+        _check(load().pf_sim_metrics(self._h, ctypes.c_void_p(m.data_ptr()), _ptr(g), _ptr(e), _stream()),
+               "pf_sim_metrics")
+        return m, g[:self.n_req], e[:self.n_req]
+
+    def device_error(self):
+        code, idx = _i32(), _i32()
+        ctx = load().pf_sim_context(self._h)
+        _check(load().pf_get_device_error(ctx, ctypes.byref(code), ctypes.byref(idx), _stream()),
+               "pf_get_device_error")
+        return code.value, idx.value
 
 
 def _wrap_device_int32(ptr: int, count: int) -> torch.Tensor:

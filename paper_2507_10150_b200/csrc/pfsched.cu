@@ -1,6 +1,7 @@
 // pfsched.cu — the C-ABI of libpfsched.so (include/pfsched.h): context, argument
 // validation, and launches of the sm_100a kernels in pf_history.cuh / pf_admit.cuh.
 // No torch types cross this boundary; every array is a caller-owned device pointer.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -11,6 +12,7 @@
 #include "pf_admit.cuh"  // defines PF_BPT, PF_MINMAX, PF_LOCKSTEP_MAX
 #include "pf_baseline.cuh"
 #include "pf_history.cuh"
+#include "pf_sim.cuh"
 
 namespace {
 
@@ -489,6 +491,228 @@ pf_status pf_export_history(pf_ctx* c, int32_t* rows_out, void* stream) {
   pf::export_rows_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(c->ring, c->head, c->n_rows,
                                                                        c->row_window, rows_out);
   PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------ simulator (NEXT-2)
+struct pf_sim {
+  pf_sim_config cfg;
+  pf_ctx* ctx = nullptr;
+  int n = 0, n_req = 0;
+  uint32_t t = 0;  // iteration index = the admission tick (C-8)
+  int32_t* max_new = nullptr;
+  int32_t* bufs[24] = {nullptr};
+  int nbufs = 0;
+  long long* metrics = nullptr;
+  int32_t* counter = nullptr;
+  pf::SimState st;
+};
+
+static void free_sim(pf_sim* m) {
+  if (!m) return;
+  for (int b = 0; b < m->nbufs; ++b) cudaFree(m->bufs[b]);
+  cudaFree(m->metrics);
+  cudaFree(m->counter);
+  if (m->ctx) free_ctx(m->ctx);
+  delete m;
+}
+
+pf_status pf_sim_create(const pf_sim_config* cfg, const int32_t* req_off,
+                        const int32_t* req_input, const int32_t* req_output,
+                        const int32_t* max_new, const int32_t* capacity,
+                        const int32_t* init_history, void* stream, pf_sim** out) {
+  if (!cfg || !out || !req_off || !req_input || !req_output || !max_new || !capacity)
+    return fail(PF_EINVAL, "pf_sim_create: NULL required pointer");
+  *out = nullptr;
+  const pf_sim_config& C = *cfg;
+  if (C.n_instances < 1) return fail(PF_EINVAL, "pf_sim_create: n_instances must be >= 1");
+  if (C.policy < PF_SIM_PAST_FUTURE || C.policy > PF_SIM_CONSERVATIVE)
+    return fail(PF_EINVAL, "pf_sim_create: unknown policy %d", C.policy);
+  const bool pf_like = C.policy == PF_SIM_PAST_FUTURE || C.policy == PF_SIM_OPTIMUM;
+  if (pf_like ? (C.param_bp < 0 || C.param_bp > 9999) : C.param_bp < 1)
+    return fail(PF_EINVAL, "pf_sim_create: param_bp out of range for the policy");
+  if (C.max_input_len < 0 || C.max_len < 1 || C.max_input_len > (1 << 30) - C.max_len)
+    return fail(PF_EINVAL, "pf_sim_create: bad max_len / max_input_len");
+  cudaStream_t s = S(stream);
+  const int n = C.n_instances;
+  // host validation of the request lists (create may synchronise)
+  std::vector<int32_t> ro(n + 1), mn(n), cp(n);
+  PF_CUDA(cudaMemcpyAsync(ro.data(), req_off, (n + 1) * 4, cudaMemcpyDeviceToHost, s));
+  PF_CUDA(cudaMemcpyAsync(mn.data(), max_new, n * 4, cudaMemcpyDeviceToHost, s));
+  PF_CUDA(cudaMemcpyAsync(cp.data(), capacity, n * 4, cudaMemcpyDeviceToHost, s));
+  PF_CUDA(cudaStreamSynchronize(s));
+  if (ro[0] != 0) return fail(PF_EINVAL, "pf_sim_create: req_off[0] must be 0");
+  for (int i = 0; i < n; ++i)
+    if (ro[i + 1] < ro[i]) return fail(PF_EINVAL, "pf_sim_create: req_off decreasing at %d", i);
+  const int N = ro[n];
+  std::vector<int32_t> lp(N), L(N);
+  if (N > 0) {
+    PF_CUDA(cudaMemcpyAsync(lp.data(), req_input, (size_t)N * 4, cudaMemcpyDeviceToHost, s));
+    PF_CUDA(cudaMemcpyAsync(L.data(), req_output, (size_t)N * 4, cudaMemcpyDeviceToHost, s));
+    PF_CUDA(cudaStreamSynchronize(s));
+  }
+  for (int i = 0; i < n; ++i) {
+    if (mn[i] < 1 || mn[i] > C.max_len) return fail(PF_EINVAL, "pf_sim_create: max_new[%d] out of range", i);
+    for (int j = ro[i]; j < ro[i + 1]; ++j) {
+      if (lp[j] < 0 || lp[j] > C.max_input_len || L[j] < 1 || L[j] > mn[i])
+        return fail(PF_EINVAL, "pf_sim_create: request %d of instance %d out of range", j - ro[i], i);
+      if ((int64_t)lp[j] + L[j] > cp[i])
+        return fail(PF_EINVAL, "pf_sim_create: request %d of instance %d exceeds capacity", j - ro[i], i);
+    }
+  }
+  pf_config pc;
+  memset(&pc, 0, sizeof(pc));
+  pc.n_instances = n;
+  pc.window = C.window;
+  pc.max_len = C.max_len;
+  pc.max_input_len = C.max_input_len + C.max_len;  // queued l_p + generated (S-3)
+  pc.max_entries = C.max_entries;
+  pc.instance_base = C.instance_base;
+  pc.mode = C.mode;
+  pc.quantile_u = C.quantile_u;
+  pc.repetitions = C.repetitions;
+  pc.reserved_bp = pf_like ? C.param_bp : 0;
+  pc.seed = C.seed;
+  pc.nranks = 1;
+  pf_sim* m = new pf_sim();
+  m->cfg = C;
+  m->n = n;
+  m->n_req = N;
+  pf_status st = pf_create(&pc, init_history, stream, &m->ctx);
+  if (st != PF_OK) { free_sim(m); return st; }
+  const int E = C.max_entries;
+  const int64_t nE = (int64_t)n * E;
+  auto alloc = [&](int64_t elems) -> int32_t* {
+    int32_t* p = nullptr;
+    if (cudaMalloc(&p, (size_t)std::max<int64_t>(elems, 1) * 4 + 16) != cudaSuccess) return nullptr;
+    m->bufs[m->nbufs++] = p;
+    return p;
+  };
+  pf::SimState& S_ = m->st;
+  S_.n = n;
+  S_.E = E;
+  int32_t* req_off_d = alloc(n + 1);
+  int32_t* lp_d = alloc(N);
+  int32_t* L_d = alloc(N);
+  int32_t* cap_d = alloc(n);
+  m->max_new = alloc(n);
+  S_.gen = alloc(N);
+  S_.evc = alloc(N);
+  S_.qbuf = alloc(N);
+  S_.qhead = alloc(n);
+  S_.qlen = alloc(n);
+  S_.run_ids = alloc(nE);
+  S_.run_k = alloc(n);
+  S_.done = alloc(n);
+  S_.comp_tmp = alloc(nE);
+  S_.cnt = alloc(3LL * n);
+  S_.off = alloc(3LL * (n + 1));
+  S_.comp_len = alloc(nE);
+  S_.c_lp = alloc(nE);
+  S_.c_gen = alloc(nE);
+  S_.c_lhat = alloc(nE);
+  S_.q_lp = alloc(nE);
+  S_.q_lhat = alloc(nE);
+  S_.admitted = alloc(n);
+  bool ok = m->nbufs == 23;
+  for (int b = 0; b < m->nbufs; ++b) ok = ok && m->bufs[b] != nullptr;
+  ok = ok && cudaMalloc(&m->metrics, (size_t)n * pf::SIM_NMETRICS * 8) == cudaSuccess;
+  ok = ok && cudaMalloc(&m->counter, 16) == cudaSuccess;
+  if (!ok) { free_sim(m); return fail(PF_ENOMEM, "pf_sim_create: device allocation failed"); }
+  S_.req_off = req_off_d;
+  S_.req_lp = lp_d;
+  S_.req_L = L_d;
+  S_.capacity = cap_d;
+  S_.metrics = m->metrics;
+  S_.err = m->ctx->err;
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMemcpyAsync(req_off_d, req_off, (n + 1) * 4, cudaMemcpyDeviceToDevice, s);
+  if (N > 0) {
+    e = e ? e : cudaMemcpyAsync(lp_d, req_input, (size_t)N * 4, cudaMemcpyDeviceToDevice, s);
+    e = e ? e : cudaMemcpyAsync(L_d, req_output, (size_t)N * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  e = e ? e : cudaMemcpyAsync(cap_d, capacity, n * 4, cudaMemcpyDeviceToDevice, s);
+  e = e ? e : cudaMemcpyAsync(m->max_new, max_new, n * 4, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) { free_sim(m); return fail(PF_ECUDA, "pf_sim_create: %s", cudaGetErrorString(e)); }
+  pf::sim_init_kernel<<<(n + 127) / 128, 128, 0, s>>>(S_);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) { free_sim(m); return fail(PF_ECUDA, "pf_sim_create: %s", cudaGetErrorString(e)); }
+  *out = m;
+  return PF_OK;
+}
+
+pf_status pf_sim_step(pf_sim* m, int32_t iterations, void* stream) {
+  if (!m) return fail(PF_EINVAL, "pf_sim_step: NULL sim");
+  if (iterations < 0) return fail(PF_EINVAL, "pf_sim_step: iterations must be >= 0");
+  cudaStream_t s = S(stream);
+  const pf::SimState& st = m->st;
+  const int n = m->n, n1 = n + 1;
+  const int wblocks = (int)(((int64_t)n * 32 + 255) / 256);
+  int32_t* comp_off = st.off;
+  int32_t* run_off = st.off + n1;
+  int32_t* q_off = st.off + 2 * n1;
+  for (int32_t it = 0; it < iterations; ++it, ++m->t) {
+    pf::sim_finish_kernel<<<wblocks, 256, 0, s>>>(st);
+    pf::sim_scan_kernel<<<1, 1024, 0, s>>>(n, st.cnt, st.off);
+    pf::sim_gather_kernel<<<wblocks, 256, 0, s>>>(st);
+    PF_CUDA(cudaGetLastError());
+    pf_status r = PF_OK;
+    switch (m->cfg.policy) {
+      case PF_SIM_PAST_FUTURE:
+        r = pf_update_history(m->ctx, comp_off, st.comp_len, 1, stream);
+        if (r == PF_OK)
+          r = launch_admit(m->ctx, run_off, st.c_lp, st.c_gen, q_off, st.q_lp, m->max_new,
+                           st.capacity, m->t, st.admitted, st.comp_tmp /* peak: scratch */,
+                           nullptr, nullptr, nullptr, s);
+        break;
+      case PF_SIM_OPTIMUM:
+        r = launch_admit(m->ctx, run_off, st.c_lp, st.c_gen, q_off, st.q_lp, nullptr,
+                         st.capacity, 0, st.admitted, st.comp_tmp, nullptr, nullptr, nullptr, s,
+                         st.c_lhat, st.q_lhat);
+        break;
+      default:
+        r = pf_admit_baseline(m->ctx, m->cfg.policy == PF_SIM_AGGRESSIVE ? PF_POLICY_AGGRESSIVE
+                                                                          : PF_POLICY_CONSERVATIVE,
+                              m->cfg.param_bp, run_off, st.c_lp, st.c_gen, q_off, st.q_lp,
+                              m->max_new, st.capacity, st.admitted, nullptr, stream);
+    }
+    if (r != PF_OK) return r;
+    pf::sim_apply_kernel<<<wblocks, 256, 0, s>>>(st);
+    PF_CUDA(cudaGetLastError());
+  }
+  return PF_OK;
+}
+
+pf_status pf_sim_done(pf_sim* m, int32_t* n_done, void* stream) {
+  if (!m || !n_done) return fail(PF_EINVAL, "pf_sim_done: NULL argument");
+  cudaStream_t s = S(stream);
+  pf::sim_count_done_kernel<<<1, 1024, 0, s>>>(m->n, m->st.done, m->counter);
+  PF_CUDA(cudaGetLastError());
+  PF_CUDA(cudaMemcpyAsync(n_done, m->counter, 4, cudaMemcpyDeviceToHost, s));
+  PF_CUDA(cudaStreamSynchronize(s));
+  return PF_OK;
+}
+
+pf_status pf_sim_metrics(pf_sim* m, int64_t* metrics_out, int32_t* generated_out,
+                         int32_t* evictions_out, void* stream) {
+  if (!m || !metrics_out) return fail(PF_EINVAL, "pf_sim_metrics: NULL argument");
+  cudaStream_t s = S(stream);
+  PF_CUDA(cudaMemcpyAsync(metrics_out, m->metrics, (size_t)m->n * pf::SIM_NMETRICS * 8,
+                          cudaMemcpyDeviceToDevice, s));
+  if (generated_out && m->n_req > 0)
+    PF_CUDA(cudaMemcpyAsync(generated_out, m->st.gen, (size_t)m->n_req * 4, cudaMemcpyDeviceToDevice, s));
+  if (evictions_out && m->n_req > 0)
+    PF_CUDA(cudaMemcpyAsync(evictions_out, m->st.evc, (size_t)m->n_req * 4, cudaMemcpyDeviceToDevice, s));
+  return PF_OK;
+}
+
+pf_ctx* pf_sim_context(pf_sim* m) { return m ? m->ctx : nullptr; }
+
+pf_status pf_sim_destroy(pf_sim* m) {
+  if (!m) return fail(PF_EINVAL, "pf_sim_destroy: NULL sim");
+  cudaDeviceSynchronize();
+  free_sim(m);
   return PF_OK;
 }
 

@@ -67,3 +67,26 @@ def test_null_arguments(lib):
     assert lib.pf_admit(*([None] * 8), 0, *([None] * 6)) == -1
     assert lib.pf_estimate_peak(None, None, None, None, None, 0, None, None, None) == -1
     assert lib.pf_update_history(None, None, None, 0, None) == -1
+
+
+def test_sim_null_arguments(lib):
+    assert lib.pf_sim_create(None, *([None] * 7), None) == -1
+    assert lib.pf_sim_step(None, 1, None) == -1
+    assert lib.pf_sim_done(None, None, None) == -1
+    assert lib.pf_sim_metrics(None, None, None, None, None) == -1
+    assert lib.pf_sim_destroy(None) == -1
+    assert lib.pf_sim_context(None) is None
+
+
+@pytest.mark.parametrize("kw", [dict(n_instances=0), dict(policy=9), dict(policy=0, param_bp=10000),
+                                dict(policy=2, param_bp=0), dict(max_len=0)])
+def test_sim_host_validation(lib, kw):
+    from paper_2507_10150_b200.binding import PFSimConfig
+    base = dict(n_instances=2, window=16, max_len=64, max_input_len=64, max_entries=16, policy=0,
+                param_bp=300, mode=0, quantile_u=0, repetitions=1, seed=0, instance_base=0)
+    base.update(kw)
+    cfg = PFSimConfig(**base)
+    h = ctypes.c_void_p()
+    dummy = ctypes.c_void_p(16)  # never dereferenced: the config is rejected first
+    assert lib.pf_sim_create(ctypes.byref(cfg), *([dummy] * 5), None, None, ctypes.byref(h)) == -1
+    assert h.value is None
