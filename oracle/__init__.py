@@ -20,7 +20,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "pf_oracle.cpp")
-_SRCS = [_SRC, os.path.join(_HERE, "pf_sim_oracle.cpp")]
+_SRCS = [_SRC, os.path.join(_HERE, "pf_sim_oracle.cpp"), os.path.join(_HERE, "pf_analysis_oracle.cpp")]
 _LIB_PATH = os.path.join(_HERE, "liborc.so")
 _lib = None
 
@@ -125,6 +125,13 @@ def lib():
         L.orc_sim_run.restype = None
         L.orc_sim_run.argtypes = [ctypes.POINTER(_SimArgs), ctypes.c_int32]
         L.orc_sizeof_sim_args.restype = ctypes.c_int32
+        F64P = ctypes.POINTER(ctypes.c_double)
+        L.orc_window_similarity.restype = ctypes.c_int32
+        L.orc_window_similarity.argtypes = [I32P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, I64P,
+                                            F64P, F64P]
+        L.orc_adjacent_similarity.restype = ctypes.c_int32
+        L.orc_adjacent_similarity.argtypes = [I32P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_int32, F64P, F64P]
         assert L.orc_sizeof_sim_args() == ctypes.sizeof(_SimArgs), "oracle sim ABI struct mismatch"
         _lib = L
     return _lib
@@ -326,3 +333,33 @@ def sim_run(*, req_off, req_input, req_output, max_new, capacity, policy, param_
                     met.ctypes.data_as(I64P), _p32(gen), _p32(ev))
     lib().orc_sim_run(ctypes.byref(args), n_threads or os.cpu_count() or 1)
     return met, gen[:n_req], ev[:n_req]
+
+
+# ---------------------------------------------------------------- window similarity (NEXT-3)
+def window_similarity(lengths, window: int, max_len: int):
+    """-> (gram [B, B] int64, cos [B, B] float64, (mean_adjacent, mean_global)) or None."""
+    x = _i32(lengths)
+    B = len(x) // window if window > 0 else 0
+    if B < 2:
+        return None
+    g = np.empty((B, B), np.int64)
+    c = np.empty((B, B), np.float64)
+    sm = np.empty(2, np.float64)
+    F = ctypes.POINTER(ctypes.c_double)
+    got = lib().orc_window_similarity(_p32(x), len(x), window, max_len, g.ctypes.data_as(I64P),
+                                      c.ctypes.data_as(F), sm.ctypes.data_as(F))
+    return None if got == 0 else (g, c, (float(sm[0]), float(sm[1])))
+
+
+def adjacent_similarity(lengths, hist_window: int, run_window: int, max_len: int):
+    """-> (cos per running window [K] float64, mean) or None."""
+    x = _i32(lengths)
+    if hist_window < 1 or run_window < 1 or len(x) < hist_window + run_window:
+        return None
+    K = (len(x) - hist_window) // run_window
+    c = np.empty(K, np.float64)
+    mean = ctypes.c_double()
+    F = ctypes.POINTER(ctypes.c_double)
+    got = lib().orc_adjacent_similarity(_p32(x), len(x), hist_window, run_window, max_len,
+                                        c.ctypes.data_as(F), ctypes.byref(mean))
+    return None if got == 0 else (c, mean.value)

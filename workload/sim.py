@@ -48,3 +48,20 @@ def make_sim_workload(cls: int, n_inst: int, n_req: int, *, div: int = 1, slots:
         "max_len": max_new,
         "max_input_len": max_in,
     }
+
+
+F_STREAM_B, F_STREAM = 46, 47
+
+
+def make_length_stream(classes, per_class: int, *, div: int = 1, seed: int = 0x2507101500000200):
+    """A synthetic trace of output lengths for the window-similarity analysis (NEXT-3):
+    ``per_class`` requests of each class in ``classes`` concatenated in order (the paper's
+    varying-load workload, PAPER.md:383), lengths // div clamped to ≥ 1. -> int32 tensor."""
+    parts = []
+    for s, cls in enumerate(classes):
+        ids = torch.arange(per_class, dtype=torch.int64) + s * per_class
+        c = torch.full_like(ids, cls)
+        x1 = _draw(_key(seed, ids, F_STREAM_B), torch.zeros_like(ids))
+        x2 = _draw(_key(seed, ids, F_STREAM), torch.zeros_like(ids))
+        parts.append((_lengths(c, x1, x2, "L") // div).clamp(min=1))
+    return torch.cat(parts).to(torch.int32)
