@@ -21,7 +21,8 @@
  *                      whose M* fits the capacity M, early return at the first
  *                      failure
  *
- * Exact integer semantics (no floating point anywhere):
+ * Exact integer semantics (no floating point on the scheduling path; DESIGN.md §3 — only
+ * the NEXT-3 analysis calls report fp64 cosines of exact integer Gram entries):
  *   history     w output lengths per window, FIFO; every value in [1, Lmax] (C-1, C-2)
  *   prediction  for a request with l_t generated tokens (l_t = 0 for queued, C-16):
  *               gt = sorted{h ∈ L_h : h > l_t} (C-4 strict); if gt is empty
@@ -48,7 +49,8 @@
  *     outputs are fully overwritten; nothing is retained after the call.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream). All work is
  *     enqueued on it; no call synchronises the host except pf_create, pf_destroy,
- *     pf_get_device_error and pf_export_history.
+ *     pf_get_device_error, pf_export_history, pf_sim_create, pf_sim_done,
+ *     pf_sim_destroy and the two analysis calls (input check).
  *   - A context is not thread-safe; calls on one context must be stream-ordered.
  *   - Host-checkable problems return a negative pf_status synchronously and
  *     enqueue nothing; pf_last_error() then describes it (thread-local).
@@ -286,6 +288,30 @@ pf_status pf_sim_metrics(pf_sim* sim, int64_t* metrics_out, int32_t* generated_o
 pf_ctx* pf_sim_context(pf_sim* sim);
 
 pf_status pf_sim_destroy(pf_sim* sim);
+
+/* ------------------------------------------------------------------------------------
+ * Window-similarity analysis (fig:dist / fig:cos_win,
+ * PAPER.md:175-192): how similar the output-length distributions of request windows are.
+ * `lengths` is a device stream of output lengths in [1, max_len] (checked: PF_EINVAL;
+ * these calls synchronise `stream` for the check). Windows are consecutive,
+ * non-overlapping blocks of `window` requests, the trailing remainder dropped
+ * (fig:dist caption "1000 requests, no overlap"); h_b(l) counts length l in window b
+ * (token-exact bins).
+ *   pf_window_similarity: B = n / window >= 2 windows.
+ *     gram_out    [B × B] int64 (nullable): G[i][j] = Σ_l h_i(l)·h_j(l), exact
+ *     cos_out     [B × B] fp64  (nullable): G[i][j] / sqrt(G[i][i]·G[j][j])
+ *     summary_out [2]     fp64  (nullable): mean_i cos[i][i+1] ("diagonal"),
+ *                                           mean_{i≠j} cos[i][j] ("global")
+ *   pf_adjacent_similarity: a historical window of hist_window requests followed by a
+ *     running window of run_window: running window k = [h + k·r, h + (k+1)·r),
+ *     K = (n − h) / r; cos_out [K] fp64 = cosine of (historical_k, running_k);
+ *     mean_out [1] fp64 nullable = their mean. */
+pf_status pf_window_similarity(const int32_t* lengths, int64_t n, int32_t window, int32_t max_len,
+                               int64_t* gram_out, double* cos_out, double* summary_out,
+                               void* stream);
+pf_status pf_adjacent_similarity(const int32_t* lengths, int64_t n, int32_t hist_window,
+                                 int32_t run_window, int32_t max_len, double* cos_out,
+                                 double* mean_out, void* stream);
 
 /* Describes the last failing call on this thread ("" if none). */
 const char* pf_last_error(void);

@@ -53,7 +53,7 @@ SYMBOLS = ("pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer",
            "pf_estimate_peak", "pf_admit", "pf_admit_override", "pf_admit_baseline", "pf_get_device_error",
            "pf_clear_device_error", "pf_export_history", "pf_last_error", "pf_abi_version",
            "pf_sim_create", "pf_sim_step", "pf_sim_done", "pf_sim_metrics", "pf_sim_context",
-           "pf_sim_destroy")
+           "pf_sim_destroy", "pf_window_similarity", "pf_adjacent_similarity")
 
 
 def load(path: str = LIB_PATH):
@@ -86,6 +86,8 @@ def load(path: str = LIB_PATH):
     L.pf_sim_context.argtypes = [_vp]
     L.pf_sim_context.restype = _vp
     L.pf_sim_destroy.argtypes = [_vp]
+    L.pf_window_similarity.argtypes = [_vp, ctypes.c_int64, _i32, _i32, _vp, _vp, _vp, _vp]
+    L.pf_adjacent_similarity.argtypes = [_vp, ctypes.c_int64, _i32, _i32, _i32, _vp, _vp, _vp]
     for s in SYMBOLS:
         if s not in ("pf_abi_version", "pf_last_error", "pf_sim_context"):
             getattr(L, s).restype = _i32
@@ -295,6 +297,33 @@ class Simulator:
         _check(load().pf_get_device_error(ctx, ctypes.byref(code), ctypes.byref(idx), _stream()),
                "pf_get_device_error")
         return code.value, idx.value
+
+
+def window_similarity(lengths: torch.Tensor, window: int, max_len: int):
+    """fig:dist (NEXT-3): -> (gram [B, B] int64, cos [B, B] float64, summary [2] float64:
+    mean adjacent, mean global) on the device."""
+    B = lengths.numel() // window if window > 0 else 0
+    dev = lengths.device
+    g = torch.empty((max(B, 1), max(B, 1)), dtype=torch.int64, device=dev)
+    c = torch.empty((max(B, 1), max(B, 1)), dtype=torch.float64, device=dev)
+    sm = torch.empty(2, dtype=torch.float64, device=dev)
+    _check(load().pf_window_similarity(_ptr(lengths), lengths.numel(), window, max_len,
+                                       ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(c.data_ptr()),
+                                       ctypes.c_void_p(sm.data_ptr()), _stream()), "pf_window_similarity")
+    return g, c, sm
+
+
+def adjacent_similarity(lengths: torch.Tensor, hist_window: int, run_window: int, max_len: int):
+    """fig:cos_win (NEXT-3): -> (cos per running window [K] float64, mean [1] float64)."""
+    n = lengths.numel()
+    K = (n - hist_window) // run_window if (hist_window > 0 and run_window > 0 and n >= hist_window + run_window) else 0
+    dev = lengths.device
+    c = torch.empty(max(K, 1), dtype=torch.float64, device=dev)
+    m = torch.empty(1, dtype=torch.float64, device=dev)
+    _check(load().pf_adjacent_similarity(_ptr(lengths), n, hist_window, run_window, max_len,
+                                         ctypes.c_void_p(c.data_ptr()), ctypes.c_void_p(m.data_ptr()),
+                                         _stream()), "pf_adjacent_similarity")
+    return c[:K], m
 
 
 def _wrap_device_int32(ptr: int, count: int) -> torch.Tensor:

@@ -13,6 +13,7 @@
 #include "pf_baseline.cuh"
 #include "pf_history.cuh"
 #include "pf_sim.cuh"
+#include "pf_analysis.cuh"
 
 namespace {
 
@@ -713,6 +714,75 @@ pf_status pf_sim_destroy(pf_sim* m) {
   if (!m) return fail(PF_EINVAL, "pf_sim_destroy: NULL sim");
   cudaDeviceSynchronize();
   free_sim(m);
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------ analysis (NEXT-3)
+static pf_status check_lengths(const int32_t* x, int64_t n, int32_t max_len, cudaStream_t s,
+                               const char* who) {
+  int* flag = nullptr;
+  PF_CUDA(cudaMallocAsync(&flag, 4, s));
+  cudaMemsetAsync(flag, 0, 4, s);
+  pf::lengths_check_kernel<<<296, 256, 0, s>>>(x, n, max_len, flag);
+  int h = 0;
+  cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(flag, s);
+  PF_CUDA(cudaStreamSynchronize(s));
+  if (h) return fail(PF_EINVAL, "%s: a length is outside [1, max_len]", who);
+  return PF_OK;
+}
+
+pf_status pf_window_similarity(const int32_t* lengths, int64_t n, int32_t window, int32_t max_len,
+                               int64_t* gram_out, double* cos_out, double* summary_out,
+                               void* stream) {
+  if (!lengths) return fail(PF_EINVAL, "pf_window_similarity: NULL lengths");
+  if (window < 1 || n < 2LL * window) return fail(PF_EINVAL, "pf_window_similarity: fewer than 2 windows");
+  if (max_len < 1 || max_len > 32767) return fail(PF_ERANGE, "pf_window_similarity: max_len must be in [1, 32767]");
+  const int64_t B64 = n / window;
+  if (B64 > 46340) return fail(PF_ERANGE, "pf_window_similarity: more than 46340 windows");
+  const int B = (int)B64;
+  cudaStream_t s = S(stream);
+  pf_status st = check_lengths(lengths, B64 * window, max_len, s, "pf_window_similarity");
+  if (st != PF_OK) return st;
+  long long* G = reinterpret_cast<long long*>(gram_out);
+  double* C = cos_out;
+  if (!G) PF_CUDA(cudaMallocAsync(&G, (size_t)B * B * 8, s));
+  if (!C && summary_out) PF_CUDA(cudaMallocAsync(&C, (size_t)B * B * 8, s));
+  const size_t smem = (size_t)(max_len + 1) * 4;
+  if (smem > 48 * 1024)
+    PF_CUDA(cudaFuncSetAttribute(pf::gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  pf::gram_kernel<<<B, 512, smem, s>>>(lengths, window, B, max_len, G);
+  PF_CUDA(cudaGetLastError());
+  if (C) {
+    const int64_t t = (int64_t)B * B;
+    pf::cosine_kernel<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(G, B, C);
+    if (summary_out) pf::similarity_summary_kernel<<<1, 1024, 0, s>>>(C, B, summary_out);
+    PF_CUDA(cudaGetLastError());
+  }
+  if (!gram_out) cudaFreeAsync(G, s);
+  if (!cos_out && C) cudaFreeAsync(C, s);
+  return PF_OK;
+}
+
+pf_status pf_adjacent_similarity(const int32_t* lengths, int64_t n, int32_t hist_window,
+                                 int32_t run_window, int32_t max_len, double* cos_out,
+                                 double* mean_out, void* stream) {
+  if (!lengths || !cos_out) return fail(PF_EINVAL, "pf_adjacent_similarity: NULL argument");
+  if (hist_window < 1 || run_window < 1 || n < (int64_t)hist_window + run_window)
+    return fail(PF_EINVAL, "pf_adjacent_similarity: no running window");
+  if (max_len < 1 || max_len > 27000) return fail(PF_ERANGE, "pf_adjacent_similarity: max_len must be in [1, 27000]");
+  const int64_t K64 = (n - hist_window) / run_window;
+  if (K64 > (1LL << 31) - 1) return fail(PF_ERANGE, "pf_adjacent_similarity: too many windows");
+  const int K = (int)K64;
+  cudaStream_t s = S(stream);
+  pf_status st = check_lengths(lengths, hist_window + K64 * run_window, max_len, s, "pf_adjacent_similarity");
+  if (st != PF_OK) return st;
+  const size_t smem = (size_t)2 * (max_len + 1) * 4;
+  if (smem > 48 * 1024)
+    PF_CUDA(cudaFuncSetAttribute(pf::adjacent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  pf::adjacent_kernel<<<K, 512, smem, s>>>(lengths, hist_window, run_window, max_len, cos_out);
+  if (mean_out) pf::mean_kernel<<<1, 1024, 0, s>>>(cos_out, K, mean_out);
+  PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
 

@@ -90,3 +90,12 @@ def test_sim_host_validation(lib, kw):
     dummy = ctypes.c_void_p(16)  # never dereferenced: the config is rejected first
     assert lib.pf_sim_create(ctypes.byref(cfg), *([dummy] * 5), None, None, ctypes.byref(h)) == -1
     assert h.value is None
+
+
+def test_analysis_host_validation(lib):
+    assert lib.pf_window_similarity(None, 10, 2, 8, None, None, None, None) == -1
+    dummy = ctypes.c_void_p(16)
+    assert lib.pf_window_similarity(dummy, 3, 2, 8, None, None, None, None) == -1   # one window
+    assert lib.pf_window_similarity(dummy, 10, 2, 40000, None, None, None, None) == -2
+    assert lib.pf_adjacent_similarity(dummy, 10, 8, 4, 8, dummy, None, None) == -1  # no running window
+    assert lib.pf_adjacent_similarity(dummy, 10, 2, 2, 8, None, None, None) == -1
