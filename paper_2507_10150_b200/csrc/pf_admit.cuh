@@ -184,6 +184,47 @@ struct Team {
       sync();
     }
   }
+  // excl<NV> on unsigned words (modular adds): packed (A << 9 | N) prefix sums.
+  template <int NV>
+  __device__ __forceinline__ void excl_u(uint32_t (&v)[NV], uint32_t (&tot)[NV]) const {
+    uint32_t inc[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+      inc[c] = v[c];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc[c], d);
+        if (lane >= d) inc[c] += t;
+      }
+    }
+    if constexpr (TW == 1) {
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        tot[c] = __shfl_sync(0xffffffffu, inc[c], 31);
+        v[c] = inc[c] - v[c];
+      }
+    } else {
+      uint32_t* xu = reinterpret_cast<uint32_t*>(xs);
+      if (lane == 31) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) xu[c * TW + wid] = inc[c];
+      }
+      sync();
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        uint32_t base = 0, total = 0;
+#pragma unroll
+        for (int x = 0; x < TW; ++x) {
+          const uint32_t s = xu[c * TW + x];
+          base += (x < wid) ? s : 0u;
+          total += s;
+        }
+        v[c] = base + inc[c] - v[c];
+        tot[c] = total;
+      }
+      sync();
+    }
+  }
   __device__ __forceinline__ int max(int v) const {
     v = __reduce_max_sync(0xffffffffu, v);
     if constexpr (TW == 1) {
@@ -581,6 +622,7 @@ admit_kernel(AdmitParams p) {
     // this thread's bins in registers (16-byte shared loads)
     int bA[BPT], bN[BPT], qA[BPT], qN[BPT];
     uint32_t ed[BPT];
+    uint32_t pR = 0, pQ = 0;  // PACK: this thread's packed (A << 9 | N) sums
 #pragma unroll
     for (int x0 = 0; x0 < BPT; x0 += 4) {
       const uint4 e4 = *reinterpret_cast<const uint4*>(edges + b0 + x0);
@@ -604,6 +646,8 @@ admit_kernel(AdmitParams p) {
           qA[x0 + c] = (int)(qq[c] >> 9);
           qN[x0 + c] = (int)(qq[c] & 511u);
           ed[x0 + c] = ee[c];
+          pR += rr[c];
+          pQ += qq[c];
         }
       } else {
         const uint4 ra = *reinterpret_cast<const uint4*>(binR + b0 + x0);
@@ -622,15 +666,25 @@ admit_kernel(AdmitParams p) {
         }
       }
     }
-    int s[4] = {0, 0, 0, 0}, tot[4];
+    int s[4] = {0, 0, 0, 0};
+    if (PACK) {  // the packed fields never carry: Σ A < 2^23, Σ N < 2^9 (host PACK bound)
+      uint32_t v[2] = {pR, pQ}, t2[2];
+      T.template excl_u<2>(v, t2);
+      s[0] = (int)(v[0] >> 9);
+      s[1] = (int)(v[0] & 511u);
+      s[2] = (int)(v[1] >> 9);
+      s[3] = (int)(v[1] & 511u);
+    } else {
+      int tot[4];
 #pragma unroll
-    for (int x = 0; x < BPT; ++x) {
-      s[0] += bA[x];
-      s[1] += bN[x];
-      s[2] += qA[x];
-      s[3] += qN[x];
+      for (int x = 0; x < BPT; ++x) {
+        s[0] += bA[x];
+        s[1] += bN[x];
+        s[2] += qA[x];
+        s[3] += qN[x];
+      }
+      T.template excl<4>(s, tot);
     }
-    T.template excl<4>(s, tot);
     const int s0[4] = {s[0], s[1], s[2], s[3]};
     // walk: exact T at lower edges (lower bounds), upper bounds of wide bins
     int lb_r = 0, lb_a = 0, lb_tau = 0, lb_trun = 0, ub_r = 0, ub_a = 0;
