@@ -20,7 +20,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "pf_oracle.cpp")
-_SRCS = [_SRC, os.path.join(_HERE, "pf_sim_oracle.cpp"), os.path.join(_HERE, "pf_analysis_oracle.cpp")]
+_SRCS = [_SRC, os.path.join(_HERE, "pf_sim_oracle.cpp"), os.path.join(_HERE, "pf_analysis_oracle.cpp"),
+         os.path.join(_HERE, "pf_forward_oracle.cpp")]
 _LIB_PATH = os.path.join(_HERE, "liborc.so")
 _lib = None
 
@@ -77,6 +78,19 @@ SIM_METRICS = ("iterations", "decode_steps", "evictions", "finished", "consumed_
                "future_sum", "samples", "future_max", "forced", "admissions")
 
 
+class _ForwardArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_clusters", ctypes.c_int32), ("cluster_size", ctypes.c_int32),
+        ("windows", I32P), ("window", ctypes.c_int32),
+        ("run_off", I32P), ("input_len", I32P), ("generated", I32P),
+        ("max_new", I32P), ("capacity", I32P), ("cq_off", I32P), ("cq_input_len", I32P),
+        ("mode", ctypes.c_int32), ("quantile_u", ctypes.c_uint32), ("reserved_bp", ctypes.c_int32),
+        ("seed", ctypes.c_uint64), ("tick", ctypes.c_uint32), ("instance_base", ctypes.c_int64),
+        ("max_entries", ctypes.c_int32),
+        ("dest_out", I32P), ("forwarded_out", I32P), ("peak_out", I32P),
+    ]
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -126,6 +140,10 @@ def lib():
         L.orc_sim_run.argtypes = [ctypes.POINTER(_SimArgs), ctypes.c_int32]
         L.orc_sizeof_sim_args.restype = ctypes.c_int32
         F64P = ctypes.POINTER(ctypes.c_double)
+        L.orc_forward.restype = None
+        L.orc_forward.argtypes = [ctypes.POINTER(_ForwardArgs)]
+        L.orc_sizeof_forward_args.restype = ctypes.c_int32
+        assert L.orc_sizeof_forward_args() == ctypes.sizeof(_ForwardArgs), "oracle forward ABI mismatch"
         L.orc_window_similarity.restype = ctypes.c_int32
         L.orc_window_similarity.argtypes = [I32P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, I64P,
                                             F64P, F64P]
@@ -363,3 +381,34 @@ def adjacent_similarity(lengths, hist_window: int, run_window: int, max_len: int
     got = lib().orc_adjacent_similarity(_p32(x), len(x), hist_window, run_window, max_len,
                                         c.ctypes.data_as(F), ctypes.byref(mean))
     return None if got == 0 else (c, mean.value)
+
+
+# ---------------------------------------------------------------- forwarding (NEXT-4)
+def forward(*, cluster_size, windows, run_off, input_len, generated, max_new, capacity, cq_off,
+            cq_input_len, mode=0, quantile_u=0x80000000, reserved_bp=0, seed=0, tick=0,
+            instance_base=0, max_entries=1 << 30):
+    """Cross-instance forwarding (pf_forward_oracle.cpp, readings F-1..F-4).
+    windows: [n, w] history per instance. -> (dest [Σq], forwarded [C], peak [n])."""
+    win = np.ascontiguousarray(np.asarray(windows, dtype=np.int32))
+    n, w = win.shape
+    C = n // cluster_size
+    keep = []
+
+    def c32(x):
+        a = _i32(x)
+        if a.size == 0:
+            a = np.zeros(1, np.int32)
+        keep.append(a)
+        return a
+
+    nq = int(np.asarray(cq_off)[-1])
+    dest = np.empty(max(nq, 1), np.int32)
+    fwd = np.empty(C, np.int32)
+    peak = np.empty(n, np.int32)
+    args = _ForwardArgs(C, cluster_size, _p32(win), w, _p32(c32(run_off)), _p32(c32(input_len)),
+                        _p32(c32(generated)), _p32(c32(max_new)), _p32(c32(capacity)), _p32(c32(cq_off)),
+                        _p32(c32(cq_input_len)), mode, quantile_u & 0xFFFFFFFF, reserved_bp,
+                        seed & 0xFFFFFFFFFFFFFFFF, tick & 0xFFFFFFFF, instance_base, max_entries,
+                        _p32(dest), _p32(fwd), _p32(peak))
+    lib().orc_forward(ctypes.byref(args))
+    return dest[:nq], fwd, peak
