@@ -313,6 +313,28 @@ pf_status pf_adjacent_similarity(const int32_t* lengths, int64_t n, int32_t hist
                                  int32_t run_window, int32_t max_len, double* cos_out,
                                  double* mean_out, void* stream);
 
+/* ------------------------------------------------------------------------------------
+ * Cross-instance request forwarding by M* headroom (the paper's
+ * future work: "forward requests to underutilized services ... aiming to
+ * ensure that each service reaches full capacity"). Readings F-1..F-4:
+ * the context's n_instances are n / cluster_size clusters of cluster_size instances
+ * (instance s of cluster c = c·cluster_size + s), each cluster with one FIFO queue
+ * (cq_off [C+1], cq_input_len). Requests are forwarded in queue order; request j goes
+ * to the instance s that passes Alg.1's check 10^4·M*_s(R_s ∪ F_s ∪ {j}) ≤
+ * (10^4 − reserved_bp)·M_s with the largest headroom (ties: lowest s); the first
+ * request no instance can take stops forwarding (C-14). Predictions per instance are
+ * pf_admit's: running slots 0..k_s−1, the cluster's j-th queued request (1-based) as
+ * slot k_s + j − 1 (C-8, R = 1). Outputs: dest_out [cq_off[C]] = instance in [0, S) or
+ * −1; forwarded_out [C]; peak_out [n] = M*_s(R_s ∪ F_s). Needs a per-instance context
+ * with window <= Lmax + 1 (PF_ESTATE otherwise), cluster_size in [1, 32] dividing n,
+ * cluster_size·max_entries·8 <= 200 KB (PF_ERANGE). Data errors: the cluster's outputs
+ * are −1 and the sticky device error word is set. Enqueued on `stream`. */
+pf_status pf_forward(pf_ctx* ctx, int32_t cluster_size, const int32_t* run_off,
+                     const int32_t* input_len, const int32_t* generated, const int32_t* max_new,
+                     const int32_t* capacity, const int32_t* cq_off, const int32_t* cq_input_len,
+                     uint32_t tick, int32_t* dest_out, int32_t* forwarded_out, int32_t* peak_out,
+                     void* stream);
+
 /* Describes the last failing call on this thread ("" if none). */
 const char* pf_last_error(void);
 

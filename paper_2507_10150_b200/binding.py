@@ -53,7 +53,7 @@ SYMBOLS = ("pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer",
            "pf_estimate_peak", "pf_admit", "pf_admit_override", "pf_admit_baseline", "pf_get_device_error",
            "pf_clear_device_error", "pf_export_history", "pf_last_error", "pf_abi_version",
            "pf_sim_create", "pf_sim_step", "pf_sim_done", "pf_sim_metrics", "pf_sim_context",
-           "pf_sim_destroy", "pf_window_similarity", "pf_adjacent_similarity")
+           "pf_sim_destroy", "pf_window_similarity", "pf_adjacent_similarity", "pf_forward")
 
 
 def load(path: str = LIB_PATH):
@@ -86,6 +86,7 @@ def load(path: str = LIB_PATH):
     L.pf_sim_context.argtypes = [_vp]
     L.pf_sim_context.restype = _vp
     L.pf_sim_destroy.argtypes = [_vp]
+    L.pf_forward.argtypes = [_vp, _i32] + [_vp] * 7 + [ctypes.c_uint32] + [_vp] * 4
     L.pf_window_similarity.argtypes = [_vp, ctypes.c_int64, _i32, _i32, _vp, _vp, _vp, _vp]
     L.pf_adjacent_similarity.argtypes = [_vp, ctypes.c_int64, _i32, _i32, _i32, _vp, _vp, _vp]
     for s in SYMBOLS:
@@ -216,6 +217,21 @@ class Scheduler:
                                         _ptr(capacity), _ptr(admitted_out), _ptr(used_out), _stream()),
                "pf_admit_baseline")
         return admitted_out, used_out
+
+    def forward(self, cluster_size: int, run_off, input_len, generated, max_new, capacity, cq_off,
+                cq_input_len, tick: int):
+        """NEXT-4: forward each cluster's queue to its instances by M* headroom.
+        -> (dest [Σq] int32, forwarded [C] int32, peak [n] int32)."""
+        dev = run_off.device
+        C = self.n // cluster_size
+        dest = torch.empty(max(int(cq_input_len.numel()), 1), dtype=torch.int32, device=dev)
+        fwd = torch.empty(C, dtype=torch.int32, device=dev)
+        peak = torch.empty(self.n, dtype=torch.int32, device=dev)
+        _check(load().pf_forward(self._h, cluster_size, _ptr(run_off), _ptr(input_len), _ptr(generated),
+                                 _ptr(max_new), _ptr(capacity), _ptr(cq_off), _ptr(cq_input_len),
+                                 tick & 0xFFFFFFFF, _ptr(dest), _ptr(fwd), _ptr(peak), _stream()),
+               "pf_forward")
+        return dest[:cq_input_len.numel()], fwd, peak
 
     def device_error(self):
         code, idx = _i32(), _i32()

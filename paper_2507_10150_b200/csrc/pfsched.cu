@@ -14,6 +14,7 @@
 #include "pf_history.cuh"
 #include "pf_sim.cuh"
 #include "pf_analysis.cuh"
+#include "pf_forward.cuh"
 
 namespace {
 
@@ -782,6 +783,57 @@ pf_status pf_adjacent_similarity(const int32_t* lengths, int64_t n, int32_t hist
     PF_CUDA(cudaFuncSetAttribute(pf::adjacent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   pf::adjacent_kernel<<<K, 512, smem, s>>>(lengths, hist_window, run_window, max_len, cos_out);
   if (mean_out) pf::mean_kernel<<<1, 1024, 0, s>>>(cos_out, K, mean_out);
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------ forwarding (NEXT-4)
+pf_status pf_forward(pf_ctx* c, int32_t cluster_size, const int32_t* run_off,
+                     const int32_t* input_len, const int32_t* generated, const int32_t* max_new,
+                     const int32_t* capacity, const int32_t* cq_off, const int32_t* cq_input_len,
+                     uint32_t tick, int32_t* dest_out, int32_t* forwarded_out, int32_t* peak_out,
+                     void* stream) {
+  if (!c || !run_off || !input_len || !generated || !max_new || !capacity || !cq_off ||
+      !cq_input_len || !dest_out || !forwarded_out || !peak_out)
+    return fail(PF_EINVAL, "pf_forward: NULL required pointer");
+  const pf_config& C = c->cfg;
+  if (cluster_size < 1 || cluster_size > 32 || C.n_instances % cluster_size)
+    return fail(PF_EINVAL, "pf_forward: cluster_size must be in [1, 32] and divide n_instances");
+  if (c->layout != LAYOUT_SORTED)
+    return fail(PF_ESTATE, "pf_forward: needs per-instance windows with w <= Lmax+1");
+  if (C.mode == PF_MODE_SAMPLE && C.repetitions != 1)
+    return fail(PF_ESTATE, "pf_forward: sampling mode supports repetitions = 1");
+  const size_t smem = (size_t)cluster_size * C.max_entries * 8;
+  if (smem > 200 * 1024)
+    return fail(PF_ERANGE, "pf_forward: cluster_size * max_entries * 8 B must be <= 200 KB");
+  pf::ForwardParams P;
+  P.n_clusters = C.n_instances / cluster_size;
+  P.S = cluster_size;
+  P.E = C.max_entries;
+  P.w = C.window;
+  P.max_len = C.max_len;
+  P.max_input_len = C.max_input_len;
+  P.mode = C.mode;
+  P.bp = C.reserved_bp;
+  P.quantile_u = C.quantile_u;
+  P.tick = tick;
+  P.seed = C.seed;
+  P.instance_base = C.instance_base;
+  P.sorted = c->sorted;
+  P.run_off = run_off;
+  P.input_len = input_len;
+  P.generated = generated;
+  P.max_new = max_new;
+  P.capacity = capacity;
+  P.cq_off = cq_off;
+  P.cq_input_len = cq_input_len;
+  P.dest_out = dest_out;
+  P.forwarded_out = forwarded_out;
+  P.peak_out = peak_out;
+  P.err = c->err;
+  if (smem > 48 * 1024)
+    PF_CUDA(cudaFuncSetAttribute(pf::forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  pf::forward_kernel<<<P.n_clusters, cluster_size * 32, smem, S(stream)>>>(P);
   PF_CUDA(cudaGetLastError());
   return PF_OK;
 }

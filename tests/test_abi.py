@@ -99,3 +99,7 @@ def test_analysis_host_validation(lib):
     assert lib.pf_window_similarity(dummy, 10, 2, 40000, None, None, None, None) == -2
     assert lib.pf_adjacent_similarity(dummy, 10, 8, 4, 8, dummy, None, None) == -1  # no running window
     assert lib.pf_adjacent_similarity(dummy, 10, 2, 2, 8, None, None, None) == -1
+
+
+def test_forward_null_arguments(lib):
+    assert lib.pf_forward(None, 1, *([None] * 7), 0, *([None] * 4)) == -1
