@@ -49,6 +49,11 @@
 #ifndef PF_PREFETCH
 #define PF_PREFETCH 0
 #endif
+template <bool B>
+struct BoolTag {
+  static constexpr bool value = B;
+};
+
 template <int TW>
 struct MinMax {
   static constexpr bool on = PF_MINMAX && TW > 1;
@@ -506,23 +511,28 @@ admit_kernel(AdmitParams p) {
   const int32_t* lpQ = p.q_input_len + (q0 - k);  // indexed by slot e ≥ k
   int32_t* poR = p.pred_run_out ? p.pred_run_out + r0 : nullptr;
   int32_t* poQ = p.pred_q_out ? p.pred_q_out + (q0 - k) : nullptr;
-#pragma unroll 1
-  for (int e0 = tid; e0 < n_ent; e0 += 4 * TT) {
+  auto chunk = [&](const int e0, auto fast_tag) {
+    constexpr bool FAST = decltype(fast_tag)::value;
     int lp[4], lt[4], bq[4], lh[4];
     uint32_t u[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int e = e0 + c * TT;
-      const bool run = e < k;
-      lp[c] = (e < n_ent) ? __ldg((run ? lpR : lpQ) + e) : 0;
-      lt[c] = run ? __ldg(ltR + e) : 0;
+      if (FAST) {  // the whole chunk is running requests: no guards, no selects
+        lp[c] = __ldg(lpR + e);
+        lt[c] = __ldg(ltR + e);
+      } else {
+        const bool run = e < k;
+        lp[c] = (e < n_ent) ? __ldg((run ? lpR : lpQ) + e) : 0;
+        lt[c] = run ? __ldg(ltR + e) : 0;
+      }
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int e = e0 + c * TT;
       // l_p ∉ [0, max_input_len] or l_t ∉ [0, max_new) (unsigned compares catch < 0)
-      my_bad |= (e < n_ent) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
-                               ((unsigned)lt[c] >= (unsigned)max_new));
+      my_bad |= (FAST || e < n_ent) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
+                                       ((unsigned)lt[c] >= (unsigned)max_new));
       // keep lookups in range (outputs are dropped when bad): unsigned min maps l_t < 0 too
       lt[c] = (int)::min((unsigned)lt[c], (unsigned)(max_new - 1));
       u[c] = lowbias32(key_fold ^ ((uint32_t)e * 0x9E3779B9U));  // C-8, R = 1
@@ -566,15 +576,20 @@ admit_kernel(AdmitParams p) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int e = e0 + c * TT;
-        int32_t* po = e < k ? poR : poQ;
-        if (e < n_ent && po) po[e] = lh[c];
+        int32_t* po = (FAST || e < k) ? poR : poQ;
+        if ((FAST || e < n_ent) && po) po[e] = lh[c];
       }
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int e = e0 + c * TT;
-      if (e < n_ent) finish(e, lh[c], lt[c], lp[c], e < k);
+      if (FAST || e < n_ent) finish(e, lh[c], lt[c], lp[c], FAST || e < k);
     }
+  };
+#pragma unroll 1
+  for (int e0 = tid; e0 < n_ent; e0 += 4 * TT) {
+    if (e0 - tid + 4 * TT <= k) chunk(e0, BoolTag<true>());  // team-uniform test
+    else chunk(e0, BoolTag<false>());
   }
   }  // !override_lhat
   if (T.any(my_bad != 0)) {
