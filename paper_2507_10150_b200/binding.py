@@ -56,7 +56,7 @@ SYMBOLS = ("pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer",
            "pf_sim_destroy", "pf_window_similarity", "pf_adjacent_similarity", "pf_forward")
 
 
-def load(path: str = LIB_PATH):
+def load(path: str = os.environ.get("PFSCHED_LIB", LIB_PATH)):
     """Load libpfsched.so (raises if it has not been built)."""
     global _lib
     if _lib is not None:

@@ -287,9 +287,9 @@ struct Eval {
 //   hd[NB] u32       list heads, one per bin (built in a4 with atomicExch)
 //   binR[NBW] u32, binQ[NBW] u32: per-bin (A, N) — packed A << 9 | N when PACK, else
 //                    A in [0, NB) and N in [NB, 2·NB)
-//   xs[160] i32      scratch: reductions [0,32), pick [32,34), list size [36], candidates [40,137)
+//   xs[140] i32      scratch: reductions [0,32), pick [32,34), list size [36], candidates [40,137)
 //   table            S[w] (LOOK_SORTED) | C[Lmax+1] (LOOK_HIST)
-// CTA prefix: edges[NB] u32 shared by the teams.
+// (the per-bin r ranges `edges` are read through L1 from global memory: 512 B per launch)
 template <int TW, int LOOK, bool PACK>
 #ifndef PF_MIN_CTAS
 #define PF_MIN_CTAS 8
@@ -302,16 +302,13 @@ admit_kernel(AdmitParams p) {
   constexpr int NB = 32 * BPT * TW;
   constexpr int NBW = PACK ? NB : 2 * NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* edges = reinterpret_cast<uint32_t*>(smem_raw);
-  for (int b = threadIdx.x; b < NB; b += TEAMS * TT) edges[b] = __ldg(p.edges + b);
-  __syncthreads();
 
   Team<TW> T;
   T.id = threadIdx.x / TT;
   T.tid = threadIdx.x % TT;
   T.lane = threadIdx.x & 31;
   T.wid = T.tid >> 5;
-  unsigned char* base = smem_raw + NB * 4 + (size_t)T.id * p.team_smem;
+  unsigned char* base = smem_raw + (size_t)T.id * p.team_smem;
   uint32_t* rb = reinterpret_cast<uint32_t*>(base);
   int* av = reinterpret_cast<int*>(rb + p.ent_cap);  // unused when PACK
   uint16_t* nx = reinterpret_cast<uint16_t*>(av + (PACK ? 0 : p.ent_cap));
@@ -324,7 +321,7 @@ admit_kernel(AdmitParams p) {
   int* cand = T.xs + 40;    // [0]: count, then 6 ints per candidate (≤ 16); xs[36]: list size
   auto ent_r = [&](int e) -> int { return (int)(rb[e] & (PACK ? 0x1FFFu : 0xFFFFu)); };
   auto ent_a = [&](int e) -> int { return PACK ? (int)(rb[e] >> 13) : av[e]; };
-  int32_t* table = T.xs + 160;
+  int32_t* table = T.xs + 140;
 
   const int i = blockIdx.x * TEAMS + T.id;
   if (i >= p.n) return;
@@ -640,7 +637,7 @@ admit_kernel(AdmitParams p) {
     uint32_t pR = 0, pQ = 0;  // PACK: this thread's packed (A << 9 | N) sums
 #pragma unroll
     for (int x0 = 0; x0 < BPT; x0 += 4) {
-      const uint4 e4 = *reinterpret_cast<const uint4*>(edges + b0 + x0);
+      const uint4 e4 = __ldg(reinterpret_cast<const uint4*>(p.edges + b0 + x0));  // L1-resident
       uint32_t ee[4] = {e4.x, e4.y, e4.z, e4.w};
       if (MinMax<TW>::on) {  // actual r range of the bin's requests (when it has any)
         const uint4 n4 = *reinterpret_cast<const uint4*>(rmn + b0 + x0);

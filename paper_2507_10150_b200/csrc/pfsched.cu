@@ -280,10 +280,10 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   c->ent_cap = (C.max_entries + 7) & ~7;
   const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
   size_t team = (size_t)c->ent_cap * (c->pack ? 6 : 10) + (size_t)c->n_bins * 4 * ((PF_MINMAX && V.TW > 1) ? 3 : 1) +
-                nbw * 8 + 160 * 4 + table;
+                nbw * 8 + 140 * 4 + table;
   team = (team + 15) & ~(size_t)15;
   c->team_smem = (int)team;
-  c->admit_smem = (size_t)c->n_bins * 4 + team * teams_per_cta(V.TW);
+  c->admit_smem = team * teams_per_cta(V.TW);
   const int look = c->layout;
   if (c->admit_smem > 227 * 1024) {
     fail(PF_ERANGE, "admit kernel needs %zu B of shared memory", c->admit_smem);
@@ -291,6 +291,24 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   }
   PF_CUDA_C(cudaFuncSetAttribute(V.fn[look][c->pack], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->admit_smem));
+#ifndef PF_CARVEOUT
+#define PF_CARVEOUT 1
+#endif
+  if (PF_CARVEOUT) {
+    // Ask for the smallest shared-memory carve-out that keeps the full occupancy: the
+    // rest of the 256 KB unified L1 caches the group tables (LOOK_GROUP lookups).
+    int per_sm = 0;
+    PF_CUDA_C(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, V.fn[look][c->pack], teams_per_cta(V.TW) * V.TW * 32, c->admit_smem));
+    const size_t need = (size_t)std::max(1, per_sm) * (c->admit_smem + 1024);
+    // the driver rounds the hint up to the next supported size (KiB)
+    static const int kSizes[] = {0, 8, 16, 32, 64, 100, 132, 164, 196, 228};
+    int kib = 228;
+    for (int sz : kSizes)
+      if ((size_t)sz * 1024 >= need) { kib = sz; break; }
+    const int pct = kib * 100 / 228;
+    PF_CUDA_C(cudaFuncSetAttribute(V.fn[look][c->pack], cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  }
 #undef PF_CUDA_C
   *out = c;
   return PF_OK;
