@@ -53,6 +53,16 @@ template <bool B>
 struct BoolTag {
   static constexpr bool value = B;
 };
+template <int N>
+struct IntTag {
+  static constexpr int value = N;
+};
+// Ragged tails of the predict loop in 2- and 1-request chunks instead of a padded
+// 4-request chunk (fewer issued slots per instance, but less memory-level parallelism:
+// measured cfg5 +2.5 %, cfg4 −1 %; off).
+#ifndef PF_TAIL
+#define PF_TAIL 0
+#endif
 
 template <int TW>
 struct MinMax {
@@ -399,12 +409,13 @@ admit_kernel(AdmitParams p) {
   }
   // LOOK_SORTED coarse index over the sorted window: cidx[c] = #{S < c·2^csh}, c ≤ 64,
   // so upper_bound(S, l) is a binary search inside [cidx[l >> csh], cidx[(l >> csh) + 1]).
-  int* cidx = table + w;
+  int* cidx = table + w + 1;  // table[w] = sentinel above every l̂ (n_gt = 0 → max_new)
   int csh = 0;
   while (((p.max_len + 1) >> csh) > 64) ++csh;
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
     for (int x = tid; x < w; x += TT) table[x] = __ldg(src + x);
+    if (tid == 0) table[w] = 0x7FFFFFFF;
     T.sync();
     for (int c = tid; c <= 65; c += TT) {
       const int v = c << csh;  // lower_bound(S, v)
@@ -508,12 +519,13 @@ admit_kernel(AdmitParams p) {
   const int32_t* lpQ = p.q_input_len + (q0 - k);  // indexed by slot e ≥ k
   int32_t* poR = p.pred_run_out ? p.pred_run_out + r0 : nullptr;
   int32_t* poQ = p.pred_q_out ? p.pred_q_out + (q0 - k) : nullptr;
-  auto chunk = [&](const int e0, auto fast_tag) {
+  auto chunk = [&](const int e0, auto fast_tag, auto nc_tag) {
     constexpr bool FAST = decltype(fast_tag)::value;
-    int lp[4], lt[4], bq[4], lh[4];
-    uint32_t u[4];
+    constexpr int NC = decltype(nc_tag)::value;  // requests per thread in this chunk
+    int lp[NC], lt[NC], bq[NC], lh[NC];
+    uint32_t u[NC];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < NC; ++c) {
       const int e = e0 + c * TT;
       if (FAST) {  // the whole chunk is running requests: no guards, no selects
         lp[c] = __ldg(lpR + e);
@@ -525,7 +537,7 @@ admit_kernel(AdmitParams p) {
       }
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < NC; ++c) {
       const int e = e0 + c * TT;
       // l_p ∉ [0, max_input_len] or l_t ∉ [0, max_new) (unsigned compares catch < 0)
       my_bad |= (FAST || e < n_ent) & (((unsigned)lp[c] > (unsigned)p.max_input_len) |
@@ -547,16 +559,16 @@ admit_kernel(AdmitParams p) {
     }
     if (!draw_fast) {  // quantile mode or R ≠ 1: one uniform branch per chunk
 #pragma unroll
-      for (int c = 0; c < 4; ++c) u[c] = draw(e0 + c * TT);
+      for (int c = 0; c < NC; ++c) u[c] = draw(e0 + c * TT);
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < NC; ++c) {
       const int n_gt = w - bq[c];
       const int x = bq[c] + (int)__umulhi(u[c], (uint32_t)n_gt);
       if (LOOK == LOOK_GROUP) {
-        lh[c] = n_gt ? (int)__ldg(p.gS + (goffS + x)) : max_new;
+        lh[c] = (int)__ldg(p.gS + (goffS + x));  // n_gt = 0: x = W, S_g[W] = 0xFFFF sentinel
       } else if (LOOK == LOOK_SORTED) {
-        lh[c] = n_gt ? table[x] : max_new;
+        lh[c] = table[x];  // n_gt = 0: x = w, the sentinel
       } else {
         int lo = lt[c] + 1, len = n_gt ? p.max_len - lt[c] : 0;  // smallest L with C[L] > x
         while (len > 0) {
@@ -571,22 +583,34 @@ admit_kernel(AdmitParams p) {
     }
     if (want_pred) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < NC; ++c) {
         const int e = e0 + c * TT;
         int32_t* po = (FAST || e < k) ? poR : poQ;
         if ((FAST || e < n_ent) && po) po[e] = lh[c];
       }
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < NC; ++c) {
       const int e = e0 + c * TT;
       if (FAST || e < n_ent) finish(e, lh[c], lt[c], lp[c], FAST || e < k);
     }
   };
 #pragma unroll 1
-  for (int e0 = tid; e0 < n_ent; e0 += 4 * TT) {
-    if (e0 - tid + 4 * TT <= k) chunk(e0, BoolTag<true>());  // team-uniform test
-    else chunk(e0, BoolTag<false>());
+  for (int b0 = 0; b0 < n_ent;) {  // team-uniform chunk choice
+    const int e0 = b0 + tid, rem = n_ent - b0;
+    if (b0 + 4 * TT <= k) {
+      chunk(e0, BoolTag<true>(), IntTag<4>());
+      b0 += 4 * TT;
+    } else if (!PF_TAIL || rem > 2 * TT) {
+      chunk(e0, BoolTag<false>(), IntTag<4>());
+      b0 += 4 * TT;
+    } else if (rem > TT) {
+      chunk(e0, BoolTag<false>(), IntTag<2>());
+      b0 += 2 * TT;
+    } else {
+      chunk(e0, BoolTag<false>(), IntTag<1>());
+      b0 += TT;
+    }
   }
   }  // !override_lhat
   if (T.any(my_bad != 0)) {

@@ -227,11 +227,11 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     const int G = C.n_groups;
     PF_CUDA_C(cudaMalloc(&c->xbuf, (size_t)G * nb * 4 + 16));
     c->c_stride = (nb + 7) & ~7;
-    c->s_stride = (C.window + 7) & ~7;
+    c->s_stride = (C.window + 1 + 7) & ~7;  // S_g[W] = 0xFFFF sentinel (admit: n_gt = 0)
     PF_CUDA_C(cudaMalloc(&c->gC, (size_t)G * c->c_stride * 2 + 16));
     PF_CUDA_C(cudaMalloc(&c->gS, (size_t)G * c->s_stride * 2 + 16));
     PF_CUDA_C(cudaMemsetAsync(c->gC, 0, (size_t)G * c->c_stride * 2, s));
-    PF_CUDA_C(cudaMemsetAsync(c->gS, 0, (size_t)G * c->s_stride * 2, s));
+    PF_CUDA_C(cudaMemsetAsync(c->gS, 0xFF, (size_t)G * c->s_stride * 2, s));
     PF_CUDA_C(cudaMalloc(&c->dist_of, (size_t)C.n_instances * 4 + 16));
     PF_CUDA_C(cudaMalloc(&c->group_off, (size_t)(G + 1) * 4 + 16));
     PF_CUDA_C(cudaMemcpyAsync(c->group_off, C.group_off, (size_t)(G + 1) * 4,
@@ -275,7 +275,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
              (int64_t)C.max_entries * ((int64_t)C.max_input_len + C.max_len) < (1LL << 23) &&
              C.max_len < 8192 && (int64_t)C.max_input_len + C.max_len < (1LL << 19)) ? 1 : 0;
   size_t table = 0;
-  if (c->layout == LAYOUT_SORTED) table = (size_t)C.window * 4 + 66 * 4;  // S + coarse index
+  if (c->layout == LAYOUT_SORTED) table = (size_t)C.window * 4 + 4 + 66 * 4;  // S + sentinel + coarse index
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
   c->ent_cap = (C.max_entries + 7) & ~7;
   const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
