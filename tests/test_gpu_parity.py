@@ -196,3 +196,31 @@ def test_full_size_sampled_parity(c):
     gp = np.concatenate([g["pred_run"][ro[i]:ro[i + 1]] for i in pick])
     assert np.array_equal(gp, o["pred_run"])
     assert s.device_error() == (0, 0)
+
+
+@pytest.mark.parametrize("c", [3, 4, 5, 2])
+def test_empty_conditional_support(c):
+    # C-5: l_t at or above every history value -> l̂ = max_new. Every third running request
+    # is moved to l_t = max_new - 1 (the kernel's sentinel past the end of the window).
+    cfg = W.scaled(W.CONFIGS[c], 24)
+    b = W.make_batch(cfg)
+    for i in range(b.n):
+        r0, r1 = int(b.run_off[i]), int(b.run_off[i + 1])
+        b.generated[r0:r1:3] = int(b.max_new[i]) - 1
+    bd = b.to("cuda")
+    orc = make_oracle(b)
+    for mode in (0, 1):
+        s = make_scheduler(bd, mode=mode, bp=300)
+        o = oracle_admit(orc, b, mode=mode, bp=300, seed=7, R=1, tick=1, estimate=cfg.q[1] == 0)
+        if cfg.q[1] == 0:
+            g = gpu_estimate(s, bd, 1)
+            assert_same(g, o, ("peak", "pred_run"), f"cfg{c}")
+        else:
+            g = gpu_admit(s, bd, 1)
+            assert_same(g, o, ALL, f"cfg{c}")
+        pr = g["pred_run"]
+        for i in range(b.n):
+            r0 = int(b.run_off[i])
+            if int(b.run_off[i + 1]) > r0:
+                assert pr[r0] == int(b.max_new[i])
+        assert s.device_error() == (0, 0)
