@@ -35,6 +35,7 @@
 #endif
 // Refinement strategy switch: up to this many candidate bins the whole team walks each
 // candidate's list in lock-step; beyond it every thread refines its own candidate bins.
+// At most 16 (the candidate table in the team scratch holds 16 entries).
 #ifndef PF_LOCKSTEP_MAX
 #define PF_LOCKSTEP_MAX 16
 #endif
@@ -301,8 +302,13 @@ struct Eval {
 //   table            S[w] (LOOK_SORTED) | C[Lmax+1] (LOOK_HIST)
 // (the per-bin r ranges `edges` are read through L1 from global memory: 512 B per launch)
 template <int TW, int LOOK, bool PACK>
+// Resident 4-team CTAs per SM for one-warp teams (register cap 65536 / (128 · PF_MIN_CTAS)):
+// 9 → 56 registers, measured best on cfg5 (8: −4 %, 10: spills, +60 %).
 #ifndef PF_MIN_CTAS
-#define PF_MIN_CTAS 8
+#define PF_MIN_CTAS 9
+#endif
+#if PF_LOCKSTEP_MAX > 16
+#error "PF_LOCKSTEP_MAX > 16 overflows the candidate table"
 #endif
 __global__ void __launch_bounds__((TW == 1 ? 4 : 1) * TW * 32, (TW == 1 ? PF_MIN_CTAS : 2))
 admit_kernel(AdmitParams p) {
