@@ -299,7 +299,7 @@ struct Eval {
 //   binR[NBW] u32, binQ[NBW] u32: per-bin (A, N) — packed A << 9 | N when PACK, else
 //                    A in [0, NB) and N in [NB, 2·NB)
 //   xs[140] i32      scratch: reductions [0,32), pick [32,34), list size [36], candidates [40,137)
-//   table            S[w] (LOOK_SORTED) | C[Lmax+1] (LOOK_HIST)
+//   table            S[w+1] u16 + coarse index cidx[66] i32 (LOOK_SORTED) | C[Lmax+1] i32 (LOOK_HIST)
 // (the per-bin r ranges `edges` are read through L1 from global memory: 512 B per launch)
 template <int TW, int LOOK, bool PACK>
 // Resident 4-team CTAs per SM for one-warp teams (register cap 65536 / (128 · PF_MIN_CTAS)):
@@ -344,6 +344,7 @@ admit_kernel(AdmitParams p) {
   auto ent_r = [&](int e) -> int { return (int)(rb[e] & (PACK ? 0x1FFFu : 0xFFFFu)); };
   auto ent_a = [&](int e) -> int { return PACK ? (int)(rb[e] >> 13) : av[e]; };
   int32_t* table = T.xs + 140;
+  uint16_t* tS = reinterpret_cast<uint16_t*>(table);  // LOOK_SORTED: the window, u16 (Lmax < 2^16)
 
   const int i = blockIdx.x * TEAMS + T.id;
   if (i >= p.n) return;
@@ -421,20 +422,20 @@ admit_kernel(AdmitParams p) {
   }
   // LOOK_SORTED coarse index over the sorted window: cidx[c] = #{S < c·2^csh}, c ≤ 64,
   // so upper_bound(S, l) is a binary search inside [cidx[l >> csh], cidx[(l >> csh) + 1]).
-  int* cidx = table + w + 1;  // table[w] = sentinel above every l̂ (n_gt = 0 → max_new)
+  int* cidx = table + ((w + 2) >> 1);  // after tS[0..w]; tS[w] = sentinel above every l̂ (n_gt = 0 → max_new)
   int csh = 0;
   while (((p.max_len + 1) >> csh) > 64) ++csh;
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
-    for (int x = tid; x < w; x += TT) table[x] = __ldg(src + x);
-    if (tid == 0) table[w] = 0x7FFFFFFF;
+    for (int x = tid; x < w; x += TT) tS[x] = (uint16_t)__ldg(src + x);
+    if (tid == 0) tS[w] = 0xFFFF;
     T.sync();
     for (int c = tid; c <= 65; c += TT) {
       const int v = c << csh;  // lower_bound(S, v)
       int lo = 0, len = w;
       while (len > 0) {
         const int half = len >> 1;
-        const bool right = table[lo + half] < v;
+        const bool right = (int)tS[lo + half] < v;
         lo = right ? lo + half + 1 : lo;
         len = right ? len - half - 1 : half;
       }
@@ -564,7 +565,7 @@ admit_kernel(AdmitParams p) {
         int lo = cidx[cb], hi = cidx[cb + 1];
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if (table[mid] <= lt[c]) lo = mid + 1; else hi = mid;
+          if ((int)tS[mid] <= lt[c]) lo = mid + 1; else hi = mid;
         }
         bq[c] = lo;
       }
@@ -580,7 +581,7 @@ admit_kernel(AdmitParams p) {
       if (LOOK == LOOK_GROUP) {
         lh[c] = (int)__ldg(p.gS + (goffS + x));  // n_gt = 0: x = W, S_g[W] = 0xFFFF sentinel
       } else if (LOOK == LOOK_SORTED) {
-        lh[c] = table[x];  // n_gt = 0: x = w, the sentinel
+        lh[c] = tS[x];  // n_gt = 0: x = w, the sentinel
       } else {
         int lo = lt[c] + 1, len = n_gt ? p.max_len - lt[c] : 0;  // smallest L with C[L] > x
         while (len > 0) {

@@ -275,7 +275,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
              (int64_t)C.max_entries * ((int64_t)C.max_input_len + C.max_len) < (1LL << 23) &&
              C.max_len < 8192 && (int64_t)C.max_input_len + C.max_len < (1LL << 19)) ? 1 : 0;
   size_t table = 0;
-  if (c->layout == LAYOUT_SORTED) table = (size_t)C.window * 4 + 4 + 66 * 4;  // S + sentinel + coarse index
+  if (c->layout == LAYOUT_SORTED) table = (size_t)((C.window + 2) >> 1) * 4 + 66 * 4;  // u16 S + sentinel, coarse index
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
   c->ent_cap = (C.max_entries + 7) & ~7;
   const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
