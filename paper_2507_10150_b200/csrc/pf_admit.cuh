@@ -59,10 +59,10 @@ struct IntTag {
   static constexpr int value = N;
 };
 // Ragged tails of the predict loop in 2- and 1-request chunks instead of a padded
-// 4-request chunk (fewer issued slots per instance, but less memory-level parallelism:
-// measured cfg5 +2.5 %, cfg4 −1 %; off).
+// 4-request chunk (fewer issued slots per instance, but less memory-level parallelism):
+// on for multi-warp teams only (measured: cfg4, TW = 4, −2 %; cfg5, TW = 1, +6 %).
 #ifndef PF_TAIL
-#define PF_TAIL 0
+#define PF_TAIL 1
 #endif
 
 template <int TW>
@@ -614,7 +614,7 @@ admit_kernel(AdmitParams p) {
     if (b0 + 4 * TT <= k) {
       chunk(e0, BoolTag<true>(), IntTag<4>());
       b0 += 4 * TT;
-    } else if (!PF_TAIL || rem > 2 * TT) {
+    } else if (!PF_TAIL || TW == 1 || rem > 2 * TT) {
       chunk(e0, BoolTag<false>(), IntTag<4>());
       b0 += 4 * TT;
     } else if (rem > TT) {
