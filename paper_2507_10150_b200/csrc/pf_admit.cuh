@@ -301,7 +301,7 @@ struct Eval {
 //   xs[140] i32      scratch: reductions [0,32), pick [32,34), list size [36], candidates [40,137)
 //   table            S[w+1] u16 + coarse index cidx[66] i32 (LOOK_SORTED) | C[Lmax+1] i32 (LOOK_HIST)
 // (the per-bin r ranges `edges` are read through L1 from global memory: 512 B per launch)
-template <int TW, int LOOK, bool PACK>
+template <int TW, int LOOK, int PK>
 // Resident 4-team CTAs per SM for one-warp teams (register cap 65536 / (128 · PF_MIN_CTAS)):
 // 9 → 56 registers, measured best on cfg5 (8: −4 %, 10: spills, +60 %).
 #ifndef PF_MIN_CTAS
@@ -322,6 +322,11 @@ admit_kernel(AdmitParams p) {
   constexpr int TEAMS = (TW == 1) ? 4 : 1;
   constexpr int BPT = PF_BPT;  // bins per thread
   constexpr int NB = 32 * BPT * TW;
+  // PK = bits of the N field of a packed bin word (A << PK | N); 0 = unpacked bins and
+  // records. 9: N < 512 (max_entries < 512); 10: N < 1024 with Σ a < 2^22 (host bound).
+  constexpr bool PACK = PK != 0;
+  constexpr int NSH = PK ? PK : 9;
+  constexpr uint32_t NMASK = (1u << NSH) - 1u;
   constexpr int NBW = PACK ? NB : 2 * NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
 
@@ -496,7 +501,7 @@ admit_kernel(AdmitParams p) {
     }
     uint32_t* bins = run ? binR : binQ;
     if (PACK) {
-      atomicAdd(&bins[b], ((uint32_t)a << 9) | 1u);
+      atomicAdd(&bins[b], ((uint32_t)a << NSH) | 1u);
     } else {
       atomicAdd(&bins[b], (uint32_t)a);
       atomicAdd(&bins[NB + b], 1u);
@@ -656,8 +661,8 @@ admit_kernel(AdmitParams p) {
   auto bin_an = [&](const uint32_t* bins, int b, int& A, int& N) {
     if (PACK) {
       const uint32_t x = bins[b];
-      A = (int)(x >> 9);
-      N = (int)(x & 511u);
+      A = (int)(x >> NSH);
+      N = (int)(x & NMASK);
     } else {
       A = (int)bins[b];
       N = (int)bins[NB + b];
@@ -671,7 +676,7 @@ admit_kernel(AdmitParams p) {
     // this thread's bins in registers (16-byte shared loads)
     int bA[BPT], bN[BPT], qA[BPT], qN[BPT];
     uint32_t ed[BPT];
-    uint32_t pR = 0, pQ = 0;  // PACK: this thread's packed (A << 9 | N) sums
+    uint32_t pR = 0, pQ = 0;  // PACK: this thread's packed (A << NSH | N) sums
 #pragma unroll
     for (int x0 = 0; x0 < BPT; x0 += 4) {
       const uint4 e4 = __ldg(reinterpret_cast<const uint4*>(p.edges + b0 + x0));  // L1-resident
@@ -690,10 +695,10 @@ admit_kernel(AdmitParams p) {
         const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w}, qq[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          bA[x0 + c] = (int)(rr[c] >> 9);
-          bN[x0 + c] = (int)(rr[c] & 511u);
-          qA[x0 + c] = (int)(qq[c] >> 9);
-          qN[x0 + c] = (int)(qq[c] & 511u);
+          bA[x0 + c] = (int)(rr[c] >> NSH);
+          bN[x0 + c] = (int)(rr[c] & NMASK);
+          qA[x0 + c] = (int)(qq[c] >> NSH);
+          qN[x0 + c] = (int)(qq[c] & NMASK);
           ed[x0 + c] = ee[c];
           pR += rr[c];
           pQ += qq[c];
@@ -716,13 +721,13 @@ admit_kernel(AdmitParams p) {
       }
     }
     int s[4] = {0, 0, 0, 0};
-    if (PACK) {  // the packed fields never carry: Σ A < 2^23, Σ N < 2^9 (host PACK bound)
+    if (PACK) {  // the packed fields never carry: Σ A < 2^(32−NSH), Σ N < 2^NSH (host PK bound)
       uint32_t v[2] = {pR, pQ}, t2[2];
       T.template excl_u<2>(v, t2);
-      s[0] = (int)(v[0] >> 9);
-      s[1] = (int)(v[0] & 511u);
-      s[2] = (int)(v[1] >> 9);
-      s[3] = (int)(v[1] & 511u);
+      s[0] = (int)(v[0] >> NSH);
+      s[1] = (int)(v[0] & NMASK);
+      s[2] = (int)(v[1] >> NSH);
+      s[3] = (int)(v[1] & NMASK);
     } else {
       int tot[4];
 #pragma unroll
@@ -957,7 +962,7 @@ admit_kernel(AdmitParams p) {
       const int b = PACK ? bin_of<NB>(ent_r(k + jx), p.bin_shift) : (int)(rb[k + jx] >> 16);
       const int a = ent_a(k + jx);
       if (PACK) {
-        atomicAdd(&binQ[b], ((uint32_t)a << 9) | 1u);
+        atomicAdd(&binQ[b], ((uint32_t)a << NSH) | 1u);
       } else {
         atomicAdd(&binQ[b], (uint32_t)a);
         atomicAdd(&binQ[NB + b], 1u);

@@ -46,13 +46,17 @@ enum Layout { LAYOUT_SORTED = 0, LAYOUT_HIST = 1, LAYOUT_GROUP = 2 };
 typedef void (*AdmitFn)(pf::AdmitParams);
 struct Variant {
   int TW, cap;       // team warps, max requests per instance served
-  AdmitFn fn[3][2];  // [lookup][pack]
+  AdmitFn fn[3][3];  // [lookup][pack]
 };
-#define PF_VARIANT(TW, CAP)                                                                      \
-  {TW, CAP,                                                                                     \
-   {{pf::admit_kernel<TW, pf::LOOK_SORTED, false>, pf::admit_kernel<TW, pf::LOOK_SORTED, true>}, \
-    {pf::admit_kernel<TW, pf::LOOK_HIST, false>, pf::admit_kernel<TW, pf::LOOK_HIST, true>},     \
-    {pf::admit_kernel<TW, pf::LOOK_GROUP, false>, pf::admit_kernel<TW, pf::LOOK_GROUP, true>}}}
+// pack index 0: unpacked; 1: A << 9 | N bins; 2: A << 10 | N bins (one-warp teams only)
+#define PF_VARIANT(TW, CAP)                                                                    \
+  {TW, CAP,                                                                                   \
+   {{pf::admit_kernel<TW, pf::LOOK_SORTED, 0>, pf::admit_kernel<TW, pf::LOOK_SORTED, 9>,       \
+     TW == 1 ? pf::admit_kernel<TW, pf::LOOK_SORTED, 10> : nullptr},                          \
+    {pf::admit_kernel<TW, pf::LOOK_HIST, 0>, pf::admit_kernel<TW, pf::LOOK_HIST, 9>,           \
+     TW == 1 ? pf::admit_kernel<TW, pf::LOOK_HIST, 10> : nullptr},                            \
+    {pf::admit_kernel<TW, pf::LOOK_GROUP, 0>, pf::admit_kernel<TW, pf::LOOK_GROUP, 9>,         \
+     TW == 1 ? pf::admit_kernel<TW, pf::LOOK_GROUP, 10> : nullptr}}}
 const Variant kVariants[] = {PF_VARIANT(1, 512), PF_VARIANT(2, 1024), PF_VARIANT(4, 2048),
                              PF_VARIANT(8, 4096)};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
@@ -270,10 +274,18 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     PF_CUDA_C(cudaMemcpy(c->edges, ed.data(), ed.size() * 4, cudaMemcpyHostToDevice));
   }
   // PACK: per-bin (A, N) fit one 32-bit word (A << 9 | N: every bin sum < 2^23, count
-  // < 2^9) and a request record fits one (r | a << 13: Lmax < 2^13, a < 2^19)
-  c->pack = (C.max_entries < 512 &&
-             (int64_t)C.max_entries * ((int64_t)C.max_input_len + C.max_len) < (1LL << 23) &&
-             C.max_len < 8192 && (int64_t)C.max_input_len + C.max_len < (1LL << 19)) ? 1 : 0;
+  // < 2^9; or A << 10 | N: sums < 2^22, counts < 2^10) and a request record fits one
+  // (r | a << 13: Lmax < 2^13, a < 2^19)
+  {
+    const bool rec = C.max_len < 8192 && (int64_t)C.max_input_len + C.max_len < (1LL << 19);
+    const int64_t amax = (int64_t)C.max_input_len + C.max_len - 1;  // a = l_p + l_t, l_t < max_new
+    if (rec && C.max_entries < 512 && (int64_t)C.max_entries * amax < (1LL << 23))
+      c->pack = 1;
+    else if (rec && V.TW == 1 && C.max_entries < 1024 && (int64_t)C.max_entries * amax < (1LL << 22))
+      c->pack = 2;
+    else
+      c->pack = 0;
+  }
   size_t table = 0;
   if (c->layout == LAYOUT_SORTED) table = (size_t)((C.window + 2) >> 1) * 4 + 66 * 4;  // u16 S + sentinel, coarse index
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
