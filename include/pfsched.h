@@ -155,7 +155,13 @@ pf_status pf_update_history(pf_ctx* ctx, const int32_t* comp_off, const int32_t*
 pf_status pf_exchange_buffer(pf_ctx* ctx, int32_t** buf, int64_t* count);
 
 /* Shared mode only: rebuild the group CDF / sorted-window tables from the
- * (all-reduced) exchange buffer. No-op in per-instance mode. */
+ * (all-reduced) exchange buffer. No-op in per-instance mode.
+ * The group tables are double-buffered: a rebuild (here, or inside
+ * pf_update_history when nranks == 1) writes the half that the most recently
+ * enqueued admit / estimate launch does NOT read, then makes it current for later
+ * launches. So tick t+1's update / exchange / commit may run on a second stream
+ * concurrently with tick t's admit, provided the rebuild for tick t+2 is ordered
+ * after tick t's admit (the caller's events; bench.py does this). */
 pf_status pf_commit_history(pf_ctx* ctx, void* stream);
 
 /* M*(R) per instance (Eq.(eq:1)-(eq:3)) after re-predicting every running

@@ -89,8 +89,11 @@ struct pf_ctx {
   int32_t* sorted = nullptr;  // LAYOUT_SORTED
   int32_t* hist = nullptr;    // LAYOUT_HIST: per instance; LAYOUT_GROUP: partial (owned shards)
   int32_t* xbuf = nullptr;    // LAYOUT_GROUP exchange buffer [G × (Lmax+1)]
-  uint16_t* gC = nullptr;  // [G × c_stride] u16
-  uint16_t* gS = nullptr;  // [G × s_stride] u16
+  uint16_t* gC = nullptr;  // [2][G × c_stride] u16, double-buffered (tbuf = the current half)
+  uint16_t* gS = nullptr;  // [2][G × s_stride] u16
+  int tbuf = 0;            // half read by admit launches; build_group_tables fills the other
+                           // half and flips, so a tick's table build may overlap the previous
+                           // tick's admit on another stream
   int c_stride = 0, s_stride = 0;
   int32_t* dist_of = nullptr;
   int32_t* group_off = nullptr;
@@ -132,9 +135,13 @@ int grid_for(int64_t total, int threads) {
 }
 
 pf_status build_group_tables(pf_ctx* c, cudaStream_t s) {
+  const int nxt = c->tbuf ^ 1;
+  const size_t G = (size_t)c->cfg.n_groups;
   pf::group_tables_kernel<256><<<c->cfg.n_groups, 256, 0, s>>>(
-      c->xbuf, c->cfg.max_len, c->cfg.window, c->c_stride, c->s_stride, c->gC, c->gS);
+      c->xbuf, c->cfg.max_len, c->cfg.window, c->c_stride, c->s_stride,
+      c->gC + nxt * G * c->c_stride, c->gS + nxt * G * c->s_stride);
   PF_CUDA(cudaGetLastError());
+  c->tbuf = nxt;
   return PF_OK;
 }
 
@@ -232,10 +239,10 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     PF_CUDA_C(cudaMalloc(&c->xbuf, (size_t)G * nb * 4 + 16));
     c->c_stride = (nb + 7) & ~7;
     c->s_stride = (C.window + 1 + 7) & ~7;  // S_g[W] = 0xFFFF sentinel (admit: n_gt = 0)
-    PF_CUDA_C(cudaMalloc(&c->gC, (size_t)G * c->c_stride * 2 + 16));
-    PF_CUDA_C(cudaMalloc(&c->gS, (size_t)G * c->s_stride * 2 + 16));
-    PF_CUDA_C(cudaMemsetAsync(c->gC, 0, (size_t)G * c->c_stride * 2, s));
-    PF_CUDA_C(cudaMemsetAsync(c->gS, 0xFF, (size_t)G * c->s_stride * 2, s));
+    PF_CUDA_C(cudaMalloc(&c->gC, 2 * (size_t)G * c->c_stride * 2 + 16));
+    PF_CUDA_C(cudaMalloc(&c->gS, 2 * (size_t)G * c->s_stride * 2 + 16));
+    PF_CUDA_C(cudaMemsetAsync(c->gC, 0, 2 * (size_t)G * c->c_stride * 2, s));
+    PF_CUDA_C(cudaMemsetAsync(c->gS, 0xFF, 2 * (size_t)G * c->s_stride * 2, s));
     PF_CUDA_C(cudaMalloc(&c->dist_of, (size_t)C.n_instances * 4 + 16));
     PF_CUDA_C(cudaMalloc(&c->group_off, (size_t)(G + 1) * 4 + 16));
     PF_CUDA_C(cudaMemcpyAsync(c->group_off, C.group_off, (size_t)(G + 1) * 4,
@@ -402,8 +409,8 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.ent_cap = c->ent_cap;
   p.sorted = c->sorted;
   p.hist = c->hist;
-  p.gC = c->gC;
-  p.gS = c->gS;
+  p.gC = c->gC ? c->gC + (size_t)c->tbuf * C.n_groups * c->c_stride : nullptr;
+  p.gS = c->gS ? c->gS + (size_t)c->tbuf * C.n_groups * c->s_stride : nullptr;
   p.c_stride = c->c_stride;
   p.s_stride = c->s_stride;
   p.dist_of = c->dist_of;
