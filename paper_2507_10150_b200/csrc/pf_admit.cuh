@@ -98,6 +98,7 @@ struct AdmitParams {
   const uint16_t* gC;        // LOOK_GROUP  [G × c_stride]: C_g[l] = #{h ≤ l} (u16, W < 2^16)
   const uint16_t* gS;        // LOOK_GROUP  [G × s_stride]: sorted group window (u16)
   int c_stride, s_stride;    // row strides (multiples of 8 elements)
+  int csh;                   // LOOK_SORTED: coarse-index bucket width 2^csh (64 buckets)
   const int32_t* dist_of;    // LOOK_GROUP  [n]
   const int32_t* group_off;  // LOOK_GROUP  [G+1]
   // inputs
@@ -253,6 +254,27 @@ struct Team {
       for (int x = 1; x < TW; ++x) m = ::max(m, xs[x]);
       sync();
       return m;
+    }
+  }
+  // team maxima of NV values in one cross-warp exchange (one barrier pair)
+  template <int NV>
+  __device__ __forceinline__ void maxn(int (&v)[NV]) const {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) v[c] = __reduce_max_sync(0xffffffffu, v[c]);
+    if constexpr (TW > 1) {
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) xs[c * TW + wid] = v[c];
+      }
+      sync();
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        int m = xs[c * TW];
+#pragma unroll
+        for (int x = 1; x < TW; ++x) m = ::max(m, xs[c * TW + x]);
+        v[c] = m;
+      }
+      sync();
     }
   }
   __device__ __forceinline__ bool any(bool b) const {
@@ -428,8 +450,12 @@ admit_kernel(AdmitParams p) {
   // LOOK_SORTED coarse index over the sorted window: cidx[c] = #{S < c·2^csh}, c ≤ 64,
   // so upper_bound(S, l) is a binary search inside [cidx[l >> csh], cidx[(l >> csh) + 1]).
   int* cidx = table + ((w + 2) >> 1);  // after tS[0..w]; tS[w] = sentinel above every l̂ (n_gt = 0 → max_new)
-  int csh = 0;
-  while (((p.max_len + 1) >> csh) > 64) ++csh;
+  int csh = 0;  // smallest s with (Lmax+1) >> s ≤ 64
+  if constexpr (TW > 1) {
+    csh = p.csh;  // (host)
+  } else {
+    while (((p.max_len + 1) >> csh) > 64) ++csh;
+  }
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
     for (int x = tid; x < w; x += TT) tS[x] = (uint16_t)__ldg(src + x);
@@ -763,13 +789,26 @@ admit_kernel(AdmitParams p) {
       }
     }
     Eval ev;
-    ev.m_run = T.max(lb_r);
-    ev.m_all = T.max(lb_a);
-    ev.tau = lb_tau;
-    ev.t_run = lb_trun;
-    T.pick(lb_a == ev.m_all, ev.tau, ev.t_run);
-    const bool need_r = first && T.max(ub_r) > ev.m_run;
-    const bool need_a = !estimate_only && ev.m_all <= Cmax && T.max(ub_a) > ev.m_all;
+    bool need_r, need_a;
+    if constexpr (TW > 1) {  // the four team maxima in one barrier pair
+      int mx[4] = {lb_r, lb_a, ub_r, ub_a};
+      T.template maxn<4>(mx);
+      ev.m_run = mx[0];
+      ev.m_all = mx[1];
+      ev.tau = lb_tau;
+      ev.t_run = lb_trun;
+      T.pick(lb_a == ev.m_all, ev.tau, ev.t_run);
+      need_r = first && mx[2] > ev.m_run;
+      need_a = !estimate_only && ev.m_all <= Cmax && mx[3] > ev.m_all;
+    } else {
+      ev.m_run = T.max(lb_r);
+      ev.m_all = T.max(lb_a);
+      ev.tau = lb_tau;
+      ev.t_run = lb_trun;
+      T.pick(lb_a == ev.m_all, ev.tau, ev.t_run);
+      need_r = first && T.max(ub_r) > ev.m_run;
+      need_a = !estimate_only && ev.m_all <= Cmax && T.max(ub_a) > ev.m_all;
+    }
     if (!need_r && !need_a) return ev;
     // ---- refinement of the wide bins whose upper bound beats the current maximum
     if (tid == 0) cand[0] = 0;
@@ -889,8 +928,16 @@ admit_kernel(AdmitParams p) {
         s[3] += Nq;
       }
     }
-    best_r = ::max(best_r, T.max(vr));
-    const int ma = T.max(va);
+    int ma;
+    if constexpr (TW > 1) {
+      int mv[2] = {vr, va};
+      T.template maxn<2>(mv);
+      best_r = ::max(best_r, mv[0]);
+      ma = mv[1];
+    } else {
+      best_r = ::max(best_r, T.max(vr));
+      ma = T.max(va);
+    }
     if (ma > best_a) {
       best_a = ma;
       T.pick(va == ma, tau, trun);
