@@ -329,6 +329,10 @@ template <int TW, int LOOK, int PK>
 #ifndef PF_MIN_CTAS
 #define PF_MIN_CTAS 9
 #endif
+// One-warp teams per CTA (host and device must agree).
+#ifndef PF_TEAMS1
+#define PF_TEAMS1 4
+#endif
 // Multi-warp teams (one team per CTA): resident warps per SM the register cap aims at
 // (min CTAs = PF_MW_WARPS / TW). cfg4 (TW = 4): 28 → 7 CTAs, 73 registers; measured
 // 2 CTAs (the old bound, ~110 registers, 4-5 resident) 1.29 ms → 8 CTAs 0.96 ms.
@@ -338,10 +342,10 @@ template <int TW, int LOOK, int PK>
 #if PF_LOCKSTEP_MAX > 16
 #error "PF_LOCKSTEP_MAX > 16 overflows the candidate table"
 #endif
-__global__ void __launch_bounds__((TW == 1 ? 4 : 1) * TW * 32, (TW == 1 ? PF_MIN_CTAS : (PF_MW_WARPS / TW > 1 ? PF_MW_WARPS / TW : 1)))
+__global__ void __launch_bounds__((TW == 1 ? PF_TEAMS1 : 1) * TW * 32, (TW == 1 ? PF_MIN_CTAS : (PF_MW_WARPS / TW > 1 ? PF_MW_WARPS / TW : 1)))
 admit_kernel(AdmitParams p) {
   constexpr int TT = TW * 32;
-  constexpr int TEAMS = (TW == 1) ? 4 : 1;
+  constexpr int TEAMS = (TW == 1) ? PF_TEAMS1 : 1;
   constexpr int BPT = PF_BPT;  // bins per thread
   constexpr int NB = 32 * BPT * TW;
   // PK = bits of the N field of a packed bin word (A << PK | N); 0 = unpacked bins and

@@ -60,7 +60,7 @@ struct Variant {
 const Variant kVariants[] = {PF_VARIANT(1, 512), PF_VARIANT(2, 1024), PF_VARIANT(4, 2048),
                              PF_VARIANT(8, 4096)};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
-inline int teams_per_cta(int TW) { return TW == 1 ? 4 : 1; }
+inline int teams_per_cta(int TW) { return TW == 1 ? PF_TEAMS1 : 1; }
 
 // Host copy of the kernel's log-linear bin map f(r) (pf_admit.cuh header), with
 // 2^KO sub-bins per octave (KO = log2(4·PF_BPT/2)): width-1 bins for r ≤ 2^(KO+1),
