@@ -541,6 +541,15 @@ struct pf_sim {
   pf_ctx* ctx = nullptr;
   int n = 0, n_req = 0;
   uint32_t t = 0;  // iteration index = the admission tick (C-8)
+  // CUDA graphs of 1 and 8 iterations, captured on first use on a private stream. The
+  // admission tick is a kernel parameter: before each replay the admit nodes' ticks are
+  // set (cudaGraphExecKernelNodeSetParams), so the hot admit kernel is unchanged.
+  cudaStream_t cap = nullptr;
+  cudaGraph_t gr1 = nullptr, gr8 = nullptr;      // kept alive: their node handles are used
+  cudaGraphExec_t g1 = nullptr, g8 = nullptr;
+  std::vector<cudaGraphNode_t> adm1, adm8;          // admit nodes in iteration order
+  std::vector<cudaKernelNodeParams> kp1, kp8;       // their launch configuration
+  std::vector<pf::AdmitParams> prm1, prm8;          // and parameters
   int32_t* max_new = nullptr;
   int32_t* bufs[24] = {nullptr};
   int nbufs = 0;
@@ -551,6 +560,11 @@ struct pf_sim {
 
 static void free_sim(pf_sim* m) {
   if (!m) return;
+  if (m->g1) cudaGraphExecDestroy(m->g1);
+  if (m->g8) cudaGraphExecDestroy(m->g8);
+  if (m->gr1) cudaGraphDestroy(m->gr1);
+  if (m->gr8) cudaGraphDestroy(m->gr8);
+  if (m->cap) cudaStreamDestroy(m->cap);
   for (int b = 0; b < m->nbufs; ++b) cudaFree(m->bufs[b]);
   cudaFree(m->metrics);
   cudaFree(m->counter);
@@ -683,44 +697,141 @@ pf_status pf_sim_create(const pf_sim_config* cfg, const int32_t* req_off,
   return PF_OK;
 }
 
-pf_status pf_sim_step(pf_sim* m, int32_t iterations, void* stream) {
-  if (!m) return fail(PF_EINVAL, "pf_sim_step: NULL sim");
-  if (iterations < 0) return fail(PF_EINVAL, "pf_sim_step: iterations must be >= 0");
-  cudaStream_t s = S(stream);
+namespace {
+// One simulator iteration (six launches) with admission tick m->t.
+pf_status sim_iteration(pf_sim* m, cudaStream_t s) {
   const pf::SimState& st = m->st;
   const int n = m->n, n1 = n + 1;
   const int wblocks = (int)(((int64_t)n * 32 + 255) / 256);
   int32_t* comp_off = st.off;
   int32_t* run_off = st.off + n1;
   int32_t* q_off = st.off + 2 * n1;
-  for (int32_t it = 0; it < iterations; ++it, ++m->t) {
-    pf::sim_finish_kernel<<<wblocks, 256, 0, s>>>(st);
-    pf::sim_scan_kernel<<<1, 1024, 0, s>>>(n, st.cnt, st.off);
-    pf::sim_gather_kernel<<<wblocks, 256, 0, s>>>(st);
-    PF_CUDA(cudaGetLastError());
-    pf_status r = PF_OK;
-    switch (m->cfg.policy) {
-      case PF_SIM_PAST_FUTURE:
-        r = pf_update_history(m->ctx, comp_off, st.comp_len, 1, stream);
-        if (r == PF_OK)
-          r = launch_admit(m->ctx, run_off, st.c_lp, st.c_gen, q_off, st.q_lp, m->max_new,
-                           st.capacity, m->t, st.admitted, st.comp_tmp /* peak: scratch */,
-                           nullptr, nullptr, nullptr, s);
-        break;
-      case PF_SIM_OPTIMUM:
-        r = launch_admit(m->ctx, run_off, st.c_lp, st.c_gen, q_off, st.q_lp, nullptr,
-                         st.capacity, 0, st.admitted, st.comp_tmp, nullptr, nullptr, nullptr, s,
-                         st.c_lhat, st.q_lhat);
-        break;
-      default:
-        r = pf_admit_baseline(m->ctx, m->cfg.policy == PF_SIM_AGGRESSIVE ? PF_POLICY_AGGRESSIVE
-                                                                          : PF_POLICY_CONSERVATIVE,
-                              m->cfg.param_bp, run_off, st.c_lp, st.c_gen, q_off, st.q_lp,
-                              m->max_new, st.capacity, st.admitted, nullptr, stream);
+  pf::sim_finish_kernel<<<wblocks, 256, 0, s>>>(st);
+  pf::sim_scan_kernel<<<1, 1024, 0, s>>>(n, st.cnt, st.off);
+  pf::sim_gather_kernel<<<wblocks, 256, 0, s>>>(st);
+  PF_CUDA(cudaGetLastError());
+  pf_status r = PF_OK;
+  switch (m->cfg.policy) {
+    case PF_SIM_PAST_FUTURE:
+      r = pf_update_history(m->ctx, comp_off, st.comp_len, 1, s);
+      if (r == PF_OK)
+        r = launch_admit(m->ctx, run_off, st.c_lp, st.c_gen, q_off, st.q_lp, m->max_new,
+                         st.capacity, m->t, st.admitted, st.comp_tmp /* peak: scratch */,
+                         nullptr, nullptr, nullptr, s);
+      break;
+    case PF_SIM_OPTIMUM:
+      r = launch_admit(m->ctx, run_off, st.c_lp, st.c_gen, q_off, st.q_lp, nullptr,
+                       st.capacity, 0, st.admitted, st.comp_tmp, nullptr, nullptr, nullptr, s,
+                       st.c_lhat, st.q_lhat);
+      break;
+    default:
+      r = pf_admit_baseline(m->ctx, m->cfg.policy == PF_SIM_AGGRESSIVE ? PF_POLICY_AGGRESSIVE
+                                                                        : PF_POLICY_CONSERVATIVE,
+                            m->cfg.param_bp, run_off, st.c_lp, st.c_gen, q_off, st.q_lp,
+                            m->max_new, st.capacity, st.admitted, nullptr, s);
+  }
+  if (r != PF_OK) return r;
+  pf::sim_apply_kernel<<<wblocks, 256, 0, s>>>(st);
+  PF_CUDA(cudaGetLastError());
+  return PF_OK;
+}
+
+// Capture `iters` iterations into an executable graph; collect the past-future admit
+// kernel nodes (in capture order = iteration order) and their parameters.
+pf_status sim_capture(pf_sim* m, int iters, cudaGraph_t* graph, cudaGraphExec_t* out,
+                      std::vector<cudaGraphNode_t>& nodes, std::vector<cudaKernelNodeParams>& kps,
+                      std::vector<pf::AdmitParams>& prms) {
+  PF_CUDA(cudaStreamBeginCapture(m->cap, cudaStreamCaptureModeThreadLocal));
+  pf_status r = PF_OK;
+  for (int u = 0; u < iters && r == PF_OK; ++u) r = sim_iteration(m, m->cap);
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(m->cap, &g);
+  if (r != PF_OK) {
+    if (g) cudaGraphDestroy(g);
+    return r;
+  }
+  PF_CUDA(e);
+  nodes.clear();
+  kps.clear();
+  prms.clear();
+  if (m->cfg.policy == PF_SIM_PAST_FUTURE) {
+    const void* fn = reinterpret_cast<const void*>(kVariants[m->ctx->variant].fn[m->ctx->layout][m->ctx->pack]);
+    // walk the (linear) chain from its root in dependency order
+    size_t nn = 0;
+    cudaGraphGetRootNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> cur(nn);
+    cudaGraphGetRootNodes(g, cur.data(), &nn);
+    while (!cur.empty()) {
+      cudaGraphNode_t nd = cur[0];
+      cudaGraphNodeType ty;
+      cudaGraphNodeGetType(nd, &ty);
+      if (ty == cudaGraphNodeTypeKernel) {
+        cudaKernelNodeParams kp;
+        if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == fn) {
+          nodes.push_back(nd);
+          prms.push_back(*reinterpret_cast<pf::AdmitParams*>(kp.kernelParams[0]));
+          kp.kernelParams = nullptr;
+          kp.extra = nullptr;
+          kps.push_back(kp);
+        }
+      }
+      size_t nd_n = 0;
+      cudaGraphNodeGetDependentNodes(nd, nullptr, &nd_n);
+      cur.resize(nd_n);
+      if (nd_n) cudaGraphNodeGetDependentNodes(nd, cur.data(), &nd_n);
     }
+    if ((int)nodes.size() != iters) {
+      cudaGraphDestroy(g);
+      return fail(PF_ECUDA, "pf_sim_step: found %d admit nodes in a %d-iteration graph", (int)nodes.size(), iters);
+    }
+  }
+  const cudaError_t e2 = cudaGraphInstantiate(out, g, 0);
+  if (e2 != cudaSuccess) cudaGraphDestroy(g);
+  PF_CUDA(e2);
+  *graph = g;
+  return PF_OK;
+}
+
+pf_status sim_replay(pf_sim* m, cudaGraphExec_t ex, std::vector<cudaGraphNode_t>& nodes,
+                     std::vector<cudaKernelNodeParams>& kps, std::vector<pf::AdmitParams>& prms,
+                     cudaStream_t s) {
+  for (size_t u = 0; u < nodes.size(); ++u) {  // the ticks of this replay's iterations
+    prms[u].tick = m->t + (uint32_t)u;
+    void* args[1] = {&prms[u]};
+    cudaKernelNodeParams kp = kps[u];
+    kp.kernelParams = args;
+    PF_CUDA(cudaGraphExecKernelNodeSetParams(ex, nodes[u], &kp));
+  }
+  PF_CUDA(cudaGraphLaunch(ex, s));
+  return PF_OK;
+}
+}  // namespace
+
+pf_status pf_sim_step(pf_sim* m, int32_t iterations, void* stream) {
+  if (!m) return fail(PF_EINVAL, "pf_sim_step: NULL sim");
+  if (iterations < 0) return fail(PF_EINVAL, "pf_sim_step: iterations must be >= 0");
+  cudaStream_t s = S(stream);
+  if (iterations < 4) {  // a few iterations: plain launches
+    for (int32_t it = 0; it < iterations; ++it, ++m->t) {
+      pf_status r = sim_iteration(m, s);
+      if (r != PF_OK) return r;
+    }
+    return PF_OK;
+  }
+  // CUDA-graph replays: 8-iteration graphs, then single-iteration ones
+  if (!m->g1) {
+    PF_CUDA(cudaStreamCreateWithFlags(&m->cap, cudaStreamNonBlocking));
+    pf_status r = sim_capture(m, 1, &m->gr1, &m->g1, m->adm1, m->kp1, m->prm1);
+    if (r == PF_OK) r = sim_capture(m, 8, &m->gr8, &m->g8, m->adm8, m->kp8, m->prm8);
     if (r != PF_OK) return r;
-    pf::sim_apply_kernel<<<wblocks, 256, 0, s>>>(st);
-    PF_CUDA(cudaGetLastError());
+  }
+  for (; iterations >= 8; iterations -= 8, m->t += 8) {
+    pf_status r = sim_replay(m, m->g8, m->adm8, m->kp8, m->prm8, s);
+    if (r != PF_OK) return r;
+  }
+  for (; iterations > 0; --iterations, ++m->t) {
+    pf_status r = sim_replay(m, m->g1, m->adm1, m->kp1, m->prm1, s);
+    if (r != PF_OK) return r;
   }
   return PF_OK;
 }

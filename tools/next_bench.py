@@ -87,7 +87,7 @@ def main():
         dt = time.perf_counter() - t0
         m = sim.metrics()[0].sum(0).tolist()
         emit(f"NEXT-2 simulator {name:15s} 256 x 200 D1 requests: {it} iterations in {dt:.2f} s = "
-             f"{it / dt:.0f} iterations/s, {m[0] / dt:.3g} instance-iterations/s (launch-bound: 6 launches/iter)")
+             f"{it / dt:.0f} iterations/s, {m[0] / dt:.3g} instance-iterations/s (CUDA-graph replays, 6 kernels/iter)")
         sim.close()
 
     # ---- NEXT-3 analysis on a BurstGPT-sized trace
