@@ -44,17 +44,43 @@ __global__ void __launch_bounds__(256) baseline_kernel(BaselineParams p) {
   else if (max_new < 1 || max_new > p.max_len) bad = PF_BAD_MAX_NEW;
   else if (cap < 0) bad = PF_BAD_CAPACITY;
   const bool cons = p.policy == POLICY_CONSERVATIVE;
-  // running requests: current consumption (aggressive) or budgets (conservative)
+  // running requests: current consumption (aggressive) or budgets (conservative). The
+  // rows are streamed 4 requests per lane per chunk with the chunk's loads issued
+  // together (no loop-carried dependence on the loaded values); a lane keeps its first
+  // data error in row order.
   int base = 0;
-  for (int e = lane; !bad && e < k; e += 32) {
-    const int l_p = p.input_len[r0 + e], l_t = p.generated[r0 + e];
-    if (l_p < 0 || l_p > p.max_input_len) bad = PF_BAD_INPUT_LEN;
-    else if (l_t < 0 || l_t >= max_new) bad = PF_BAD_GENERATED;
-    base += cons ? l_p + max_new : l_p + l_t;
-  }
-  for (int j = lane; !bad && j < q; j += 32) {
-    const int l_p = p.q_input_len[q0 + j];
-    if (l_p < 0 || l_p > p.max_input_len) bad = PF_BAD_INPUT_LEN;
+  if (!bad) {
+    int lb = 0;
+    const int32_t* lpR = p.input_len + r0;
+    const int32_t* ltR = p.generated + r0;
+#pragma unroll 1
+    for (int e0 = lane; e0 < k; e0 += 128) {
+      int lp[4], lt[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = e0 + 32 * c;
+        lp[c] = e < k ? __ldg(lpR + e) : 0;
+        lt[c] = e < k ? __ldg(ltR + e) : 0;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int code = (lp[c] < 0 || lp[c] > p.max_input_len) ? PF_BAD_INPUT_LEN
+                         : (lt[c] < 0 || lt[c] >= max_new)       ? PF_BAD_GENERATED : 0;
+        lb = lb ? lb : code;
+        base += cons ? (e0 + 32 * c < k ? lp[c] + max_new : 0) : lp[c] + lt[c];
+      }
+    }
+    const int32_t* lpQ = p.q_input_len + q0;
+#pragma unroll 1
+    for (int j0 = lane; j0 < q; j0 += 128) {
+      int lp[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) lp[c] = j0 + 32 * c < q ? __ldg(lpQ + j0 + 32 * c) : 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (!lb && (lp[c] < 0 || lp[c] > p.max_input_len)) lb = PF_BAD_INPUT_LEN;
+    }
+    bad = lb;
   }
   bad = __reduce_max_sync(0xffffffffu, bad);
   if (bad) {
