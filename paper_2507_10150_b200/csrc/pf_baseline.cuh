@@ -15,6 +15,11 @@ namespace pf {
 
 enum { POLICY_AGGRESSIVE = 1, POLICY_CONSERVATIVE = 2 };
 
+// requests per lane per chunk of the streaming loops
+#ifndef PF_BASE_NC
+#define PF_BASE_NC 4
+#endif
+
 struct BaselineParams {
   int n;
   int policy;
@@ -54,16 +59,16 @@ __global__ void __launch_bounds__(256) baseline_kernel(BaselineParams p) {
     const int32_t* lpR = p.input_len + r0;
     const int32_t* ltR = p.generated + r0;
 #pragma unroll 1
-    for (int e0 = lane; e0 < k; e0 += 128) {
-      int lp[4], lt[4];
+    for (int e0 = lane; e0 < k; e0 += 32 * PF_BASE_NC) {
+      int lp[PF_BASE_NC], lt[PF_BASE_NC];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < PF_BASE_NC; ++c) {
         const int e = e0 + 32 * c;
         lp[c] = e < k ? __ldg(lpR + e) : 0;
         lt[c] = e < k ? __ldg(ltR + e) : 0;
       }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < PF_BASE_NC; ++c) {
         const int code = (lp[c] < 0 || lp[c] > p.max_input_len) ? PF_BAD_INPUT_LEN
                          : (lt[c] < 0 || lt[c] >= max_new)       ? PF_BAD_GENERATED : 0;
         lb = lb ? lb : code;
@@ -72,12 +77,12 @@ __global__ void __launch_bounds__(256) baseline_kernel(BaselineParams p) {
     }
     const int32_t* lpQ = p.q_input_len + q0;
 #pragma unroll 1
-    for (int j0 = lane; j0 < q; j0 += 128) {
-      int lp[4];
+    for (int j0 = lane; j0 < q; j0 += 32 * PF_BASE_NC) {
+      int lp[PF_BASE_NC];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) lp[c] = j0 + 32 * c < q ? __ldg(lpQ + j0 + 32 * c) : 0;
+      for (int c = 0; c < PF_BASE_NC; ++c) lp[c] = j0 + 32 * c < q ? __ldg(lpQ + j0 + 32 * c) : 0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < PF_BASE_NC; ++c)
         if (!lb && (lp[c] < 0 || lp[c] > p.max_input_len)) lb = PF_BAD_INPUT_LEN;
     }
     bad = lb;
