@@ -147,3 +147,85 @@ def test_gpu_shared_mode_ranks_on_one_device(P):
         assert np.array_equal(_np(adm), ref["admitted"][pos])
         assert np.array_equal(_np(pk), ref["peak"][pos])
         assert s.device_error() == (0, 0)
+
+
+def _pipelined_worker(rank, world, port, out):
+    """One rank of the bench.py schedule on cuda:0: admit(t) on the main stream while
+    update(t+1) -> all-reduce(exchange buffer) -> commit runs on a side stream."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2507_10150_b200 import Scheduler
+    torch.cuda.set_device(0)
+    M = CFG.members_per_group
+    shards = owned_shards(CFG, rank, world)
+    bd = W.make_batch(CFG, rank=rank, nranks=world, shards=shards, device="cuda")
+    s = Scheduler(n_instances=bd.n, window=CFG.window, max_len=CFG.max_len,
+                  max_input_len=CFG.max_input_len, max_entries=CFG.max_entries, n_groups=CFG.n_groups,
+                  group_off=bd.group_off, members_per_group=M, member_base=rank * M // world, mode=0,
+                  reserved_bp=500, seed=11, rank=rank, nranks=world, init_history=bd.hist_rows)
+    xbuf = s.exchange_buffer()
+    dist.all_reduce(xbuf)
+    s.commit_history()
+    main, side = torch.cuda.current_stream(), torch.cuda.Stream()
+    ready, done, res = {}, {}, []
+    slow = torch.empty(1 << 24, dtype=torch.int32, device="cuda")
+
+    def tables(t):
+        with torch.cuda.stream(side):
+            if t - 2 in done:
+                side.wait_event(done.pop(t - 2))
+            co, cl = W.make_completions(CFG, t, bd.row_ids)
+            s.update_history(co.cuda(), cl.cuda())
+            dist.all_reduce(xbuf)
+            s.commit_history()
+            e = torch.cuda.Event()
+            e.record(side)
+            ready[t] = e
+
+    tables(1)
+    for t in range(1, PIPE_TICKS + 1):
+        main.wait_event(ready.pop(t))
+        slow.add_(1)
+        adm = torch.full((bd.n,), -7, dtype=torch.int32, device="cuda")
+        pk = torch.full_like(adm, -7)
+        s.admit(bd.run_off, bd.input_len, bd.generated, bd.q_off, bd.q_input_len, bd.max_new,
+                bd.capacity, t, admitted_out=adm, peak_out=pk)
+        res.append((adm, pk))
+        e = torch.cuda.Event()
+        e.record(main)
+        done[t] = e
+        if t < PIPE_TICKS:
+            tables(t + 1)
+    torch.cuda.synchronize()
+    out[rank] = (bd.inst_ids.cpu().numpy(), [(_np(a), _np(p)) for a, p in res], s.device_error())
+    dist.destroy_process_group()
+
+
+PIPE_TICKS = 4
+
+
+@pytest.mark.gpu
+def test_gpu_two_processes_pipelined_exchange():
+    """bench.py's N > 1 schedule (side-stream exchange overlapping admit, double-buffered
+    group tables) with a real all-reduce between two processes (gloo, one device):
+    every tick equals the single-rank oracle."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_pipelined_worker, args=(2, port, out), nprocs=2, join=True)
+    b = W.make_batch(CFG)
+    orc = O.Oracle(b.hist_rows.shape[0], CFG.row_window, CFG.max_len, CFG.shards, _np(b.hist_rows))
+    ids = b.inst_ids.numpy()
+    refs = []
+    for t in range(1, PIPE_TICKS + 1):
+        co, cl = W.make_completions(CFG, t, b.row_ids)
+        assert orc.update_history(_np(co), _np(cl))[0] == 0
+        refs.append(_admit(orc, b, t))
+    for rank in range(2):
+        inst, res, err = out[rank]
+        assert err == (0, 0)
+        pos = np.searchsorted(ids, inst)
+        for t, (adm, pk) in enumerate(res):
+            assert np.array_equal(adm, refs[t]["admitted"][pos]), f"rank {rank} tick {t + 1}"
+            assert np.array_equal(pk, refs[t]["peak"][pos]), f"rank {rank} tick {t + 1}"
