@@ -54,6 +54,10 @@ template <bool B>
 struct BoolTag {
   static constexpr bool value = B;
 };
+// Requests per thread per predict chunk.
+#ifndef PF_NC
+#define PF_NC 4
+#endif
 template <int N>
 struct IntTag {
   static constexpr int value = N;
@@ -646,12 +650,12 @@ admit_kernel(AdmitParams p) {
 #pragma unroll 1
   for (int b0 = 0; b0 < n_ent;) {  // team-uniform chunk choice
     const int e0 = b0 + tid, rem = n_ent - b0;
-    if (b0 + 4 * TT <= k) {
-      chunk(e0, BoolTag<true>(), IntTag<4>());
-      b0 += 4 * TT;
+    if (b0 + PF_NC * TT <= k) {
+      chunk(e0, BoolTag<true>(), IntTag<PF_NC>());
+      b0 += PF_NC * TT;
     } else if (!PF_TAIL || TW == 1 || rem > 2 * TT) {
-      chunk(e0, BoolTag<false>(), IntTag<4>());
-      b0 += 4 * TT;
+      chunk(e0, BoolTag<false>(), IntTag<PF_NC>());
+      b0 += PF_NC * TT;
     } else if (rem > TT) {
       chunk(e0, BoolTag<false>(), IntTag<2>());
       b0 += 2 * TT;
