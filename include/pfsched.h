@@ -279,7 +279,11 @@ pf_status pf_sim_create(const pf_sim_config* cfg, const int32_t* req_off,
                         const int32_t* max_new, const int32_t* capacity,
                         const int32_t* init_history, void* stream, pf_sim** out);
 
-/* Advance every instance by `iterations` iterations (finished instances idle). Enqueued. */
+/* Advance every instance by `iterations` iterations (finished instances idle). Enqueued.
+ * With iterations >= 4 the iterations are replayed from CUDA graphs of 1 and 8
+ * iterations, captured on the first such call on a private stream (the admission tick
+ * of each replay is set on the graph's admit nodes); the results are identical to
+ * plain launches. The graphs live until pf_sim_destroy. */
 pf_status pf_sim_step(pf_sim* sim, int32_t iterations, void* stream);
 
 /* Number of finished instances (synchronises `stream`). */
