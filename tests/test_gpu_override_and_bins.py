@@ -81,3 +81,28 @@ def test_bin_pileups_refine_exactly(mode, c, n, lo, hi):
     o = oracle_admit(orc, b, mode=mode, bp=0, seed=7, R=1, tick=5, estimate=estimate)
     keys = ("peak", "pred_run") if estimate else ("admitted", "peak", "peak_running", "pred_run", "pred_q")
     assert_same(g, o, keys, f"cfg{c} pileup")
+
+
+@pytest.mark.parametrize("c", [3, 5])
+def test_whole_instance_in_one_bin(c):
+    """Constant history and constant l_t: every request of an instance has the same r, so
+    one bin holds all of them (512 for cfg 3: the 10-bit count field of the packed bin
+    words is full at N = 512; cfg 5: up to 480 in a 9-bit field)."""
+    cfg = W.scaled(W.CONFIGS[c], 8)
+    b = W.make_batch(cfg)
+    b.hist_rows = torch.full(tuple(b.hist_rows.shape), 4000, dtype=torch.int32)
+    b.generated = torch.full((b.generated.numel(),), 10, dtype=torch.int32)
+    cur = torch.zeros(b.n, dtype=torch.int64).index_add_(
+        0, torch.repeat_interleave(torch.arange(b.n), torch.diff(b.run_off.long())),
+        (b.input_len + b.generated).long())
+    b.capacity = (cur * 3 // 2).to(torch.int32)
+    bd = b.to("cuda")
+    orc = make_oracle(b)
+    estimate = cfg.q[1] == 0
+    for mode in (0, 1):
+        sch = make_scheduler(bd, mode=mode, bp=0)
+        g = gpu_estimate(sch, bd, 3) if estimate else gpu_admit(sch, bd, 3)
+        o = oracle_admit(orc, b, mode=mode, bp=0, seed=7, R=1, tick=3, estimate=estimate)
+        keys = ("peak", "pred_run") if estimate else ("admitted", "peak", "peak_running", "pred_run", "pred_q")
+        assert_same(g, o, keys, f"cfg{c} one bin")
+        assert sch.device_error() == (0, 0)
