@@ -224,3 +224,21 @@ def test_empty_conditional_support(c):
             if int(b.run_off[i + 1]) > r0:
                 assert pr[r0] == int(b.max_new[i])
         assert s.device_error() == (0, 0)
+
+
+@pytest.mark.parametrize("u", [0, 1, 0x7FFFFFFF, 0xFFFFFFFF])
+@pytest.mark.parametrize("c", [2, 3, 5])
+def test_quantile_extremes(c, u):
+    # C-3: u = 0 is the smallest history value above l_t (upper_bound), u = 2^32 − 1 the
+    # largest; both ends of ⌊u·n_gt / 2^32⌋ exercised for every layout (hist / sorted / group)
+    cfg = W.scaled(W.CONFIGS[c], 24)
+    b = W.make_batch(cfg)
+    bd = b.to("cuda")
+    orc = make_oracle(b)
+    s = make_scheduler(bd, mode=1, bp=300, quantile_u=u)
+    o = oracle_admit(orc, b, mode=1, bp=300, seed=7, R=1, tick=0, quantile_u=u, estimate=cfg.q[1] == 0)
+    if cfg.q[1] == 0:
+        assert_same(gpu_estimate(s, bd, 0), o, ("peak", "pred_run"), f"cfg{c} u={u:#x}")
+    else:
+        assert_same(gpu_admit(s, bd, 0), o, ALL, f"cfg{c} u={u:#x}")
+    assert s.device_error() == (0, 0)
