@@ -106,13 +106,13 @@ def algorithmic_bytes(cfg: W.WorkloadConfig, b: W.Batch) -> int:
     return 8 * k + 4 * q + n * (H + S + O)
 
 
-def scheduler_for(cfg, bd, rank, nranks, mode, bp, seed):
+def scheduler_for(cfg, bd, rank, nranks, mode, bp, seed, nccl_id=None):
     from paper_2507_10150_b200 import Scheduler
     kw = {}
     if cfg.shared:
         M = cfg.members_per_group
         kw = dict(n_groups=cfg.n_groups, group_off=bd.group_off, members_per_group=M,
-                  member_base=rank * M // nranks)
+                  member_base=rank * M // nranks, nccl_id=nccl_id)
     else:
         kw = dict(instance_base=int(bd.inst_ids[0]))
     return Scheduler(n_instances=bd.n, window=cfg.window, max_len=cfg.max_len,
@@ -174,13 +174,109 @@ def run_reference(args, rank, world):
     value = sub.slots() / t
     sample = (f"{sub.n} evenly spaced instances of {cfg.n_instances} ({sub.slots()} request-slots) per step, "
               f"oracle admit (Alg.1 literal, tick-stepped M*), {nt} threads")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": cfg.describe(), "decisions_per_s": sub.n / t},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ launcher
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` without a torchrun environment: re-exec this script as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    n_dev = torch.cuda.device_count()
+    if n_dev and args.gpus > n_dev:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {n_dev} CUDA device(s) are visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # INIT lines show every rank joining
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execvpe(cmd[0], cmd, env)
+
+
+def dry_launch(args):
+    """The launcher path without a GPU (CPU test): every rank joins a gloo group and the
+    ranks are counted with an all-reduce."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    n = torch.ones(1)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        dist.all_reduce(n)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_launch": True, "n_gpus": world, "ranks_counted": int(n.item())}), flush=True)
+
+
+def dist_setup(args):
+    """(rank, world, local): WORLD_SIZE from torchrun; NCCL process group with device_id."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def bench_config(args, world):
+    """The workload this run times: strong scaling = BASELINE's config split over the ranks;
+    --weak = the config's instance count PER GPU (world × n instances in total)."""
+    cfg = W.CONFIGS[args.config]
+    if args.weak and world > 1:
+        cfg = W.scaled(cfg, cfg.n_instances * world)
+    return cfg
+
+
+def share_nccl_id(rank, world):
+    """Rank 0 creates the ncclUniqueId of the library-owned communicator (pf_nccl_unique_id)
+    and broadcasts its 128 bytes over the torch process group."""
+    import torch.distributed as dist
+    from paper_2507_10150_b200 import nccl_unique_id
+    buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(buf, 0)
+    return bytes(buf.cpu().tolist())
+
+
+def output_check(cfg, bd, adm, pk, pkr, estimate, bp):
+    """Properties of the timed step's outputs that hold at any size (no oracle in the timed
+    path): Alg.1's outputs are in range, M* >= current usage (tick 0 of Eq.(eq:3)), and the
+    admitted peak respects the capacity rule while M* is monotone in p."""
+    n = bd.n
+    k = (bd.run_off[1:] - bd.run_off[:-1]).long()
+    own = torch.repeat_interleave(torch.arange(n, device=bd.run_off.device), k)
+    cur = torch.zeros(n, dtype=torch.int64, device=own.device).index_add_(
+        0, own, (bd.input_len + bd.generated).long())
+    peak_r = (pk if estimate else pkr).long()
+    bad = int((peak_r < cur).sum())
+    if not estimate:
+        q = (bd.q_off[1:] - bd.q_off[:-1]).long()
+        a, p, pr = adm.long(), pk.long(), pkr.long()
+        cmax = ((10000 - bp) * bd.capacity.long()) // 10000
+        bad += int(((a < 0) | (a > q)).sum())
+        bad += int(((a > 0) & (p > cmax)).sum())          # admitted set fits
+        bad += int((p < pr).sum())                        # M* monotone in admitted requests
+        bad += int(((a == 0) & (p != pr)).sum())          # p* = 0 reports M*(R)
+        pstar0 = int((a == 0).sum()); pall = int((a == q).sum())
+        return {"violations": bad, "p_star_0": pstar0, "p_star_q": pall, "interior": n - pstar0 - pall}
+    return {"violations": bad}
 
 
 # ------------------------------------------------------------------ our arm
@@ -191,6 +287,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--weak", action="store_true", help="N>1: the config's instances per GPU (weak scaling)")
     ap.add_argument("--mode", type=int, default=0, help="0 sample (C-8 hash), 1 quantile")
     ap.add_argument("--bp", type=int, default=500, help="reserved ratio, basis points (paper: 3/5/10 %%)")
     ap.add_argument("--seed", type=int, default=0x5EED)
@@ -198,29 +295,37 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-launch", action="store_true",
+                    help="test hook: start the ranks (gloo), count them, print one line, no GPU work")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
+    if args.dry_launch:
+        return dry_launch(args)
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, rank, world)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
         return
+    if args.config == 1:
+        return run_latency(args, rank, world, local)
 
     torch.cuda.set_device(local)
-    cfg = W.CONFIGS[args.config]
+    cfg = bench_config(args, world)
     shards = owned_shards(cfg, rank, world) if cfg.shared else None
     bd = W.make_batch(cfg, rank=rank, nranks=world, device="cuda", shards=shards)
     torch.cuda.synchronize()
-    sched = scheduler_for(cfg, bd, rank, world, args.mode, args.bp, args.seed)
+    nccl_id = share_nccl_id(rank, world) if (cfg.shared and world > 1) else None
+    # cfg2's inputs (43 MB) and per-instance histograms (34 MB) fit the 126 MB L2: rotate
+    # ROT independent (context, input set) pairs so no step finds the previous one's data
+    rot = 9 if args.config == 2 else 1
+    sets = [bd] + [bd.clone() for _ in range(rot - 1)]
+    scheds = [scheduler_for(cfg, b_, rank, world, args.mode, args.bp, args.seed, nccl_id) for b_ in sets]
+    sched = scheds[0]
     pool = [W.make_completions(cfg, t, bd.row_ids) for t in range(args.tick_pool)]
     n = bd.n
     dev = "cuda"
@@ -228,33 +333,29 @@ def main():
     pk = torch.empty(n, dtype=torch.int32, device=dev)
     pkr = torch.empty(n, dtype=torch.int32, device=dev)
     estimate = cfg.q[1] == 0
-    xbuf = sched.exchange_buffer() if (cfg.shared and world > 1) else None
-    if xbuf is not None:  # pf_create left the group tables for the all-reduce
-        import torch.distributed as dist
-        dist.all_reduce(xbuf)
-        sched.commit_history()
     stream = torch.cuda.current_stream()
 
+    def admit_call(sc, b_, t):
+        if estimate:
+            sc.estimate_peak(b_.run_off, b_.input_len, b_.generated, b_.max_new, t, peak_out=pk)
+        else:
+            sc.admit(b_.run_off, b_.input_len, b_.generated, b_.q_off, b_.q_input_len, b_.max_new,
+                     b_.capacity, t, admitted_out=adm, peak_out=pk, peak_running_out=pkr)
+
     def step(t, ev=None):
+        sc, b_ = scheds[t % rot], sets[t % rot]
         co, cl = pool[t % len(pool)]
-        sched.update_history(co, cl)
-        if xbuf is not None:
-            import torch.distributed as dist
-            dist.all_reduce(xbuf)
-            sched.commit_history()
+        sc.update_history(co, cl)
         if ev is not None:
             ev[0].record(stream)
-        if estimate:
-            sched.estimate_peak(bd.run_off, bd.input_len, bd.generated, bd.max_new, t, peak_out=pk)
-        else:
-            sched.admit(bd.run_off, bd.input_len, bd.generated, bd.q_off, bd.q_input_len, bd.max_new,
-                        bd.capacity, t, admitted_out=adm, peak_out=pk, peak_running_out=pkr)
+        admit_call(sc, b_, t)
         if ev is not None:
             ev[1].record(stream)
 
-    # Shared mode (cfg 5): tick t+1's update_history / NCCL all-reduce / group tables run
-    # on a side stream while tick t's admit runs (the library double-buffers the group
-    # tables, include/pfsched.h pf_commit_history); tables(t+2) wait for admit(t).
+    # Shared mode (cfg 5): tick t+1's update_history (+ the library's NCCL all-reduce at
+    # N > 1) / group tables run on a side stream while tick t's admit runs (the library
+    # double-buffers the group tables, include/pfsched.h pf_commit_history); tables(t+2)
+    # wait for admit(t).
     pipelined = bool(cfg.shared)
     side = torch.cuda.Stream() if pipelined else None
     tab_ready, admit_done = {}, {}
@@ -265,10 +366,6 @@ def main():
                 side.wait_event(admit_done.pop(t - 2))
             co, cl = pool[t % len(pool)]
             sched.update_history(co, cl)
-            if xbuf is not None:
-                import torch.distributed as dist
-                dist.all_reduce(xbuf)
-                sched.commit_history()
             e = torch.cuda.Event()
             e.record(side)
             tab_ready[t] = e
@@ -277,27 +374,26 @@ def main():
         stream.wait_event(tab_ready.pop(t))
         if ev is not None:
             ev[0].record(stream)
-        sched.admit(bd.run_off, bd.input_len, bd.generated, bd.q_off, bd.q_input_len, bd.max_new,
-                    bd.capacity, t, admitted_out=adm, peak_out=pk, peak_running_out=pkr)
+        admit_call(sched, bd, t)
         if ev is not None:
             ev[1].record(stream)
         e = torch.cuda.Event()
         e.record(stream)
         admit_done[t] = e
 
-    def run_steps(t0, n, kev=None):
+    def run_steps(t0, n_, kev=None):
         # admit(t) is enqueued before tables(t+1): the host-side table flip happens at the
         # tables call, so admit(t) reads the half built for tick t
         if not pipelined:
-            for j in range(n):
+            for j in range(n_):
                 step(t0 + j, kev[j] if kev else None)
             return
         if t0 not in tab_ready:
             tables(t0)
-        for j in range(n):
+        for j in range(n_):
             admit_only(t0 + j, kev[j] if kev else None)
             tables(t0 + j + 1)
-        stream.wait_event(tab_ready[t0 + n])  # the timed region holds n table builds too
+        stream.wait_event(tab_ready[t0 + n_])  # the timed region holds n table builds too
 
     def barrier():
         torch.cuda.synchronize()
@@ -321,8 +417,11 @@ def main():
     clk = clocks.stop()
     step_ms = e0.elapsed_time(e1) / K
     kern_ms = sum(a.elapsed_time(b) for a, b in kev) / K
-    code, idx = sched.device_error()
-    assert code == 0, f"device error {code} at {idx}"
+    for sc in scheds:
+        code, idx = sc.device_error()
+        assert code == 0, f"device error {code} at {idx}"
+    check = output_check(cfg, sets[(args.warmup + K - 1) % rot], adm, pk, pkr, estimate, args.bp)
+    assert check["violations"] == 0, f"output check failed: {check}"
 
     # max over ranks; whole-job units
     slots_local = bd.slots()
@@ -340,13 +439,7 @@ def main():
     peak_gbs, peak_src = peaks()
     abytes = algorithmic_bytes(cfg, bd)
     achieved = abytes / (kern_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "admit_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(f"cfg{args.config}")
-        except Exception:
-            traffic = None
+    traffic, traffic_src = measured_traffic(args.config, world, args.weak)
 
     # e2e through the public API with HOST buffers (pinned), copies inside the timed region
     host = {k: getattr(bd, k).cpu().pin_memory() for k in
@@ -371,8 +464,8 @@ def main():
         with torch.cuda.stream(cs):
             if t - 2 in used:
                 cs.wait_event(used.pop(t - 2))
-            for k, v in host.items():
-                dsets[t % 2][k].copy_(v, non_blocking=True)
+            for k_, v in host.items():
+                dsets[t % 2][k_].copy_(v, non_blocking=True)
             a, b = hpool[j % len(hpool)]
             da, db = dcos[t % 2][j % len(hpool)]
             da.copy_(a, non_blocking=True)
@@ -386,10 +479,6 @@ def main():
         d = dsets[t % 2]
         da, db = dcos[t % 2][j % len(hpool)]
         sched.update_history(da, db)
-        if xbuf is not None:
-            import torch.distributed as dist
-            dist.all_reduce(xbuf)
-            sched.commit_history()
         if estimate:
             sched.estimate_peak(d["run_off"], d["input_len"], d["generated"], d["max_new"], j, peak_out=pk)
         else:
@@ -437,25 +526,35 @@ def main():
                          f"{dt:.1f} s", "decisions_per_s": rd}
 
     if rank == 0:
+        if args.config == 2:
+            l2 = (f"{rot} independent (context, input set) pairs rotated step by step: "
+                  f"{rot} x {(abytes / 1e6):.0f} MB > 3 x 126 MB L2")
+        else:
+            l2 = f"inputs {abytes / 1e9:.2f} GB per rank > 126 MB L2 (no flush needed)"
+        scaling = "weak" if (args.weak and world > 1) else "strong"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "int32", "data": "synthetic",
             "config": {"workload": cfg.describe(), "instances": int(decisions), "request_slots": int(slots),
                        "decisions_per_s": decisions / (step_ms * 1e-3), "mode": "sample" if args.mode == 0
-                       else "quantile", "reserved_bp": args.bp, "parallelism": f"instances sharded x{world}",
-                       "l2": "inputs 2.45 GB > 126 MB L2 (no flush needed)" if args.config == 5 else
-                       "see DESIGN.md", "admit_kernel_ms": kern_ms,
-                       "step": "update_history + group tables + admit" + (" + NCCL allreduce" if xbuf is not None else "")
-                       + (" (tick t+1's history/tables on a side stream, overlapping tick t's admit)" if pipelined else "")},
+                       else "quantile", "reserved_bp": args.bp,
+                       "parallelism": f"instances sharded x{world}" + (
+                           ", shared-history all-reduce by the library's NCCL communicator" if nccl_id else ""),
+                       "l2": l2, "admit_kernel_ms": kern_ms,
+                       "step": "update_history" + (" (+ NCCL all-reduce)" if nccl_id else "")
+                       + (" + group tables" if cfg.shared else "") + " + " + ("estimate_peak" if estimate else "admit")
+                       + (" (tick t+1's history/tables on a side stream, overlapping tick t's admit)" if pipelined else ""),
+                       "output_check": check},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-                         "frac": achieved / peak_gbs, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": abytes, "kernel": "admit_kernel",
                          "frac_of_8TBs_spec": achieved / 8000.0},
             "e2e": {"value": e2e_value, "unit": UNIT, "pipelined": "step t+1's H2D overlaps step t",
                     "h2d_bytes_per_step": int(h2d + h2d_c),
                     "d2h_bytes_per_step": int(d2h)},
-            "gpu_launches": 3 * K,
+            "gpu_launches": (3 if cfg.shared else 2) * K,
             "clocks": clk,
         }
         if cpu:
@@ -464,6 +563,77 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def measured_traffic(config, world, weak):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per admit launch, from the ncu
+    --set full capture of this config at N = 1 (profiles/admit_traffic.json), else None."""
+    if world > 1 and not weak:
+        return None, "not captured for a 1/N shard"
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "admit_traffic.json")))
+        e = d.get(f"cfg{config}")
+        if isinstance(e, dict):
+            return e.get("bytes"), e.get("source")
+    except Exception:
+        pass
+    return None, "no ncu capture for this config"
+
+
+def run_latency(args, rank, world, local):
+    """cfg1 (one hand-checkable instance, 8 running + 4 queued): latency per call, not a
+    bandwidth number. Times update_history + admit through the C-ABI per call (host wall
+    clock around a synchronised call, and device time by CUDA events)."""
+    torch.cuda.set_device(local)
+    b = W.config1_fixture()
+    bd = b.to("cuda")
+    cfg = b.cfg
+    from paper_2507_10150_b200 import Scheduler
+    sched = Scheduler(n_instances=1, window=cfg.window, max_len=cfg.max_len, max_input_len=cfg.max_input_len,
+                      max_entries=cfg.max_entries, mode=args.mode, reserved_bp=args.bp, seed=args.seed,
+                      init_history=bd.hist_rows.contiguous())
+    co = torch.tensor([0, 1], dtype=torch.int32, device="cuda")
+    cl = torch.tensor([1024], dtype=torch.int32, device="cuda")
+    adm = torch.empty(1, dtype=torch.int32, device="cuda")
+    pk = torch.empty_like(adm)
+    stream = torch.cuda.current_stream()
+
+    def call(t):
+        sched.update_history(co, cl)
+        sched.admit(bd.run_off, bd.input_len, bd.generated, bd.q_off, bd.q_input_len, bd.max_new,
+                    bd.capacity, t, admitted_out=adm, peak_out=pk)
+
+    for t in range(args.warmup):
+        call(t)
+    torch.cuda.synchronize()
+    K = args.steps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    e0.record(stream)
+    for t in range(K):
+        call(args.warmup + t)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1) / K
+    walls = []
+    for t in range(min(K, 200)):
+        w0 = time.perf_counter()
+        call(t)
+        torch.cuda.synchronize()
+        walls.append(time.perf_counter() - w0)
+    clk = clocks.stop()
+    sync_us = statistics.median(walls) * 1e6
+    slots = b.slots()
+    line = {"metric": METRIC, "value": slots / (dev_ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": K,
+            "warmup": args.warmup, "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic (SURVEY P-5 hand-checkable instance)",
+            "config": {"workload": cfg.describe(), "latency_us_per_call_device": dev_ms * 1e3,
+                       "latency_us_per_call_synchronous": sync_us, "admitted": int(adm.item()),
+                       "peak": int(pk.item()), "l2": "latency-bound (4 KB): not a bandwidth number"},
+            "roofline": None, "gpu_launches": 2 * K, "clocks": clk}
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

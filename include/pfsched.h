@@ -68,7 +68,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 1
+#define PF_ABI_VERSION 2
 
 typedef struct pf_ctx pf_ctx;
 
@@ -78,6 +78,7 @@ typedef enum {
   PF_ERANGE = -2,  /* declared bounds exceed what the kernels support/overflow */
   PF_ESTATE = -3,  /* call not valid in this context mode / sequence           */
   PF_ECUDA = -4,   /* a CUDA runtime call failed (message in pf_last_error)    */
+  PF_ENCCL = -5,   /* NCCL missing or an NCCL call failed (shared mode)        */
   PF_ENOMEM = -6   /* device allocation failed                                 */
 } pf_status;
 
@@ -117,7 +118,20 @@ typedef struct {
   int32_t reserved_bp;     /* reserved ratio in basis points, 0..9999 (C-13)                   */
   uint64_t seed;           /* sampling-mode seed (C-8)                                         */
   int32_t rank, nranks;    /* shared mode: this rank owns shards {s in 0..7 : s % nranks == rank} */
+  const void* nccl_unique_id; /* shared mode, nullable: a 128-byte ncclUniqueId (from
+                              pf_nccl_unique_id on one rank, the same bytes on every rank).
+                              Set: the context owns an NCCL communicator of nranks ranks
+                              (ncclCommInitRank in pf_create, collective) and
+                              pf_update_history performs the all-reduce itself (also with
+                              nranks == 1). NULL: with nranks > 1 the caller exchanges the
+                              buffer (pf_exchange_buffer / pf_commit_history). Not retained. */
 } pf_config;
+
+/* Write a fresh ncclUniqueId (128 bytes) to id_out (host memory) for
+ * pf_config.nccl_unique_id. Call on one rank and send the bytes to the others (any
+ * out-of-band channel, e.g. a torch.distributed broadcast). NCCL is loaded at run time
+ * (dlopen "libnccl.so.2", or $PFSCHED_NCCL_LIB); PF_ENCCL if it cannot be. */
+pf_status pf_nccl_unique_id(void* id_out);
 
 /* Create a context and its device history state.
  * init_history: device, oldest first, nullable (NULL ⇒ every slot = Lmax, C-2,
@@ -127,7 +141,13 @@ typedef struct {
  *   Values must lie in [1, Lmax] (checked; PF_EINVAL otherwise).
  * Host-checked: n, w, Lmax, max_entries, R, reserved_bp, mode, rank/nranks
  *   ranges, nranks divides 8, and the int32 overflow bound
- *   max_entries·(max_input_len + 2·Lmax) < 2^31. Synchronises `stream`. */
+ *   max_entries·(max_input_len + 2·Lmax) < 2^31. The admit kernel's team of warps per
+ *   instance keeps its tables in shared memory (per-instance histogram layout, w > Lmax+1:
+ *   4·(Lmax+1) B of CDF + ≤ 10 B per request + bins); every size within these bounds fits
+ *   one team (≤ 202 KB at Lmax = 32767, max_entries = 4096), and the one-warp variant packs
+ *   fewer than 4 teams per CTA when 4 do not fit in 227 KB. Shared mode with nccl_unique_id: collective over the ranks (NCCL
+ *   communicator creation + the first all-reduce); PF_ENCCL on NCCL failure.
+ *   Synchronises `stream`. */
 pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* stream,
                     pf_ctx** out);
 
@@ -143,9 +163,12 @@ pf_status pf_destroy(pf_ctx* ctx);
  * device [total]. A row containing a length ∉ [1, Lmax] is left unchanged and
  * PF_DERR_COMPLETION is recorded.
  * Shared mode: after the local update the owned-shard group histograms are
- * written to the exchange buffer; with nranks == 1 the group tables are rebuilt
- * here; with nranks > 1 the caller must sum-all-reduce the exchange buffer across
- * ranks (e.g. NCCL on `stream`) and then call pf_commit_history. */
+ * written to the exchange buffer. With a context-owned communicator
+ * (nccl_unique_id) the call is COLLECTIVE: every rank calls it in the same order, and
+ * it enqueues ncclAllReduce(sum, int32) of the buffer and the group-table rebuild on
+ * `stream` (PF_ENCCL on NCCL failure). Without one: with nranks == 1 the group tables
+ * are rebuilt here; with nranks > 1 the caller must sum-all-reduce the exchange buffer
+ * across ranks (e.g. NCCL on `stream`) and then call pf_commit_history. */
 pf_status pf_update_history(pf_ctx* ctx, const int32_t* comp_off, const int32_t* comp_len,
                             int32_t total, void* stream);
 
@@ -155,7 +178,10 @@ pf_status pf_update_history(pf_ctx* ctx, const int32_t* comp_off, const int32_t*
 pf_status pf_exchange_buffer(pf_ctx* ctx, int32_t** buf, int64_t* count);
 
 /* Shared mode only: rebuild the group CDF / sorted-window tables from the
- * (all-reduced) exchange buffer. No-op in per-instance mode.
+ * (all-reduced) exchange buffer. No-op in per-instance mode; PF_ESTATE when the
+ * context owns its communicator (pf_update_history already did it). Until the first
+ * commit of a caller-exchanged context (nranks > 1, no nccl_unique_id),
+ * pf_estimate_peak / pf_admit return PF_ESTATE.
  * The group tables are double-buffered: a rebuild (here, or inside
  * pf_update_history when nranks == 1) writes the half that the most recently
  * enqueued admit / estimate launch does NOT read, then makes it current for later

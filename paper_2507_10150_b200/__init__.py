@@ -8,9 +8,9 @@ include/pfsched.h); ``binding`` is a ctypes marshalling layer with the same name
 from .binding import (PF_MODE_QUANTILE, PF_MODE_SAMPLE, PF_POLICY_AGGRESSIVE, PF_POLICY_CONSERVATIVE,
                       PF_SIM_AGGRESSIVE, PF_SIM_CONSERVATIVE, PF_SIM_OPTIMUM, PF_SIM_PAST_FUTURE,
                       SIM_METRICS, PFError, Scheduler, Simulator, adjacent_similarity, load,
-                      window_similarity, LIB_PATH, SYMBOLS)
+                      window_similarity, LIB_PATH, SYMBOLS, nccl_unique_id)
 
 __all__ = ["Scheduler", "Simulator", "PFError", "load", "LIB_PATH", "SYMBOLS", "PF_MODE_SAMPLE",
            "PF_MODE_QUANTILE", "PF_POLICY_AGGRESSIVE", "PF_POLICY_CONSERVATIVE", "PF_SIM_PAST_FUTURE",
            "PF_SIM_OPTIMUM", "PF_SIM_AGGRESSIVE", "PF_SIM_CONSERVATIVE", "SIM_METRICS",
-           "window_similarity", "adjacent_similarity"]
+           "window_similarity", "adjacent_similarity", "nccl_unique_id"]

@@ -21,6 +21,8 @@ PF_POLICY_AGGRESSIVE, PF_POLICY_CONSERVATIVE = 1, 2
 DERR = {0: "none", 1: "completion", 2: "offsets", 3: "max_new", 4: "input_len", 5: "generated",
         6: "capacity", 7: "override"}
 
+ABI_VERSION = 2
+NCCL_UNIQUE_ID_BYTES = 128
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
 
@@ -31,7 +33,7 @@ class PFConfig(ctypes.Structure):
         ("max_entries", _i32), ("n_groups", _i32), ("group_off", _vp), ("instance_base", ctypes.c_int64),
         ("members_per_group", _i32), ("member_base", _i32), ("mode", _i32),
         ("quantile_u", ctypes.c_uint32), ("repetitions", _i32), ("reserved_bp", _i32),
-        ("seed", ctypes.c_uint64), ("rank", _i32), ("nranks", _i32),
+        ("seed", ctypes.c_uint64), ("rank", _i32), ("nranks", _i32), ("nccl_unique_id", _vp),
     ]
 
 
@@ -49,7 +51,7 @@ SIM_METRICS = ("iterations", "decode_steps", "evictions", "finished", "consumed_
                "future_sum", "samples", "future_max", "forced", "admissions")
 
 _lib = None
-SYMBOLS = ("pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer", "pf_commit_history",
+SYMBOLS = ("pf_nccl_unique_id", "pf_create", "pf_destroy", "pf_update_history", "pf_exchange_buffer", "pf_commit_history",
            "pf_estimate_peak", "pf_admit", "pf_admit_override", "pf_admit_baseline", "pf_get_device_error",
            "pf_clear_device_error", "pf_export_history", "pf_last_error", "pf_abi_version",
            "pf_sim_create", "pf_sim_step", "pf_sim_done", "pf_sim_metrics", "pf_sim_context",
@@ -67,6 +69,7 @@ def load(path: str = os.environ.get("PFSCHED_LIB", LIB_PATH)):
     P = ctypes.POINTER
     L.pf_abi_version.restype = _i32
     L.pf_last_error.restype = ctypes.c_char_p
+    L.pf_nccl_unique_id.argtypes = [_vp]
     L.pf_create.argtypes = [P(PFConfig), _vp, _vp, P(_vp)]
     L.pf_destroy.argtypes = [_vp]
     L.pf_update_history.argtypes = [_vp, _vp, _vp, _i32, _vp]
@@ -92,7 +95,7 @@ def load(path: str = os.environ.get("PFSCHED_LIB", LIB_PATH)):
     for s in SYMBOLS:
         if s not in ("pf_abi_version", "pf_last_error", "pf_sim_context"):
             getattr(L, s).restype = _i32
-    assert L.pf_abi_version() == 1
+    assert L.pf_abi_version() == ABI_VERSION, f"{path}: ABI {L.pf_abi_version()} != {ABI_VERSION} (rebuild)"
     _lib = L
     return L
 
@@ -118,20 +121,35 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def nccl_unique_id() -> bytes:
+    """pf_nccl_unique_id: a fresh 128-byte ncclUniqueId (send it to every rank)."""
+    buf = ctypes.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    _check(load().pf_nccl_unique_id(buf), "pf_nccl_unique_id")
+    return buf.raw
+
+
 class Scheduler:
-    """One pf_ctx: device history state for n instances (or G shared groups)."""
+    """One pf_ctx: device history state for n instances (or G shared groups).
+    nccl_id (shared mode): the 128-byte ncclUniqueId of a context-owned communicator; the
+    context then all-reduces the group histograms itself inside update_history."""
 
     def __init__(self, *, n_instances: int, window: int, max_len: int, max_input_len: int,
                  max_entries: int, n_groups: int = 0, group_off: Optional[torch.Tensor] = None,
                  instance_base: int = 0, members_per_group: int = 0, member_base: int = 0,
                  mode: int = PF_MODE_SAMPLE, quantile_u: int = 0x80000000, repetitions: int = 1,
                  reserved_bp: int = 0, seed: int = 0, rank: int = 0, nranks: int = 1,
-                 init_history: Optional[torch.Tensor] = None):
+                 init_history: Optional[torch.Tensor] = None, nccl_id: Optional[bytes] = None):
         L = load()
+        idbuf = None
+        if nccl_id is not None:
+            if len(nccl_id) != NCCL_UNIQUE_ID_BYTES:
+                raise PFError("nccl_id must be 128 bytes (pf_nccl_unique_id)")
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), NCCL_UNIQUE_ID_BYTES)
         self.cfg = PFConfig(n_instances, window, max_len, max_input_len, max_entries, n_groups,
                             None if group_off is None else group_off.data_ptr(), instance_base,
                             members_per_group, member_base, mode, quantile_u & 0xFFFFFFFF,
-                            repetitions, reserved_bp, seed & 0xFFFFFFFFFFFFFFFF, rank, nranks)
+                            repetitions, reserved_bp, seed & 0xFFFFFFFFFFFFFFFF, rank, nranks,
+                            None if idbuf is None else ctypes.cast(idbuf, _vp))
         self._keep = (group_off, init_history)
         h = ctypes.c_void_p()
         _check(L.pf_create(ctypes.byref(self.cfg), _ptr(init_history), _stream(), ctypes.byref(h)),

@@ -93,6 +93,7 @@ struct AdmitParams {
   int64_t instance_base;
   int members_per_group, member_base;
   int team_smem;       // bytes of shared memory per team
+  int teams;           // teams per CTA (one-warp teams: ≤ PF_TEAMS1, fewer for large tables)
   int ent_cap;         // request slots per team (>= max_entries)
   int bin_shift;            // s of the r -> bin map (bin_of)
   const uint32_t* edges;   // [n_bins]: lo | hi << 16 (0 = no r maps to the bin)
@@ -349,7 +350,6 @@ template <int TW, int LOOK, int PK>
 __global__ void __launch_bounds__((TW == 1 ? PF_TEAMS1 : 1) * TW * 32, (TW == 1 ? PF_MIN_CTAS : (PF_MW_WARPS / TW > 1 ? PF_MW_WARPS / TW : 1)))
 admit_kernel(AdmitParams p) {
   constexpr int TT = TW * 32;
-  constexpr int TEAMS = (TW == 1) ? PF_TEAMS1 : 1;
   constexpr int BPT = PF_BPT;  // bins per thread
   constexpr int NB = 32 * BPT * TW;
   // PK = bits of the N field of a packed bin word (A << PK | N); 0 = unpacked bins and
@@ -381,7 +381,7 @@ admit_kernel(AdmitParams p) {
   int32_t* table = T.xs + 140;
   uint16_t* tS = reinterpret_cast<uint16_t*>(table);  // LOOK_SORTED: the window, u16 (Lmax < 2^16)
 
-  const int i = blockIdx.x * TEAMS + T.id;
+  const int i = blockIdx.x * (TW == 1 ? p.teams : 1) + T.id;
   if (i >= p.n) return;
   const int tid = T.tid;
   const bool estimate_only = (p.q_off == nullptr);

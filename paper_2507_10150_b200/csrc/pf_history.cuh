@@ -156,9 +156,14 @@ __global__ void update_sorted_kernel(int n_rows, int w, int max_len, const int32
   if (lane == 0) head[row] = h;
 }
 
-// Rings feeding histograms: per-instance (w > Lmax+1, rows_per_hist = 1, plain
-// stores) or shared groups (rows_per_hist = shards owned, atomics since several
-// shard rows of one group update its histogram concurrently). Warp per row.
+// Rings feeding histograms: per-instance (w > Lmax+1, rows_per_hist = 1) or shared
+// groups (rows_per_hist = shards owned). Warp per row, all lanes busy: applying c
+// completions in order to a FIFO of w slots leaves the last m = min(c, w) of them at
+// slots (head + c − m + j) mod w, j ∈ [0, m), and evicts exactly the old contents of
+// those slots (the first c − m new values are appended and evicted again: no net
+// change). Slots are distinct across j, so lane j reads its old value, writes its
+// new value and moves one count from old to new, in any order; histogram counts
+// use atomics (several lanes, and several shard rows of one group, hit one row).
 __global__ void update_hist_kernel(int n_rows, int row_window, int rows_per_hist, int max_len,
                                    const int32_t* comp_off, const int32_t* comp_len,
                                    int32_t* ring, int32_t* head, int32_t* hist, int* err) {
@@ -171,51 +176,67 @@ __global__ void update_hist_kernel(int n_rows, int row_window, int rows_per_hist
     if (lane == 0) raise_error(err, PF_BAD_COMPLETION, row);
     return;
   }
-  if (lane != 0) return;
-  int32_t* R = ring + (int64_t)row * row_window;
+  const int w = row_window, c = c1 - c0, m = min(c, w);
+  int32_t* R = ring + (int64_t)row * w;
   int32_t* H = hist + (int64_t)(row / rows_per_hist) * (max_len + 1);
-  int h = head[row];
-  for (int t = c0; t < c1; ++t) {
-    const int v_new = comp_len[t];
-    const int v_old = R[h];
-    R[h] = v_new;
-    h = (h + 1 == row_window) ? 0 : h + 1;
-    if (rows_per_hist == 1) {
-      H[v_old] -= 1;
-      H[v_new] += 1;
-    } else {
+  const int h = head[row];
+  const int first = (int)(((int64_t)h + c - m) % w);  // slot of the first surviving value
+  for (int j = lane; j < m; j += 32) {
+    int pos = first + j;
+    if (pos >= w) pos -= w;
+    const int v_new = comp_len[c1 - m + j];
+    const int v_old = R[pos];
+    R[pos] = v_new;
+    if (v_new != v_old) {
       atomicSub(&H[v_old], 1);
       atomicAdd(&H[v_new], 1);
     }
   }
-  head[row] = h;
+  if (lane == 0) head[row] = (int)(((int64_t)h + c) % w);
 }
 
 // Group tables from the (all-reduced) group histogram H_g: C_g[l] = Σ_{l'≤l} H_g[l']
-// and the sorted window S_g (S_g[x] = l for x ∈ [C_g[l−1], C_g[l])), both u16 (W < 2^16,
-// Lmax < 2^15) with row strides c_stride / s_stride. CTA per group.
+// and the sorted window S_g (S_g[x] = min{l : C_g[l] > x}), both u16 (W < 2^16,
+// Lmax < 2^15) with row strides c_stride / s_stride. Grid (G, SPLIT): every CTA of a
+// group scans the group's histogram into shared memory (coalesced, T per pass); split 0
+// stores C_g; split z fills S_g[x] for its x-range by a binary search in the shared copy
+// (one independent search per entry, no serial per-bin loops). Shared memory: 4·(Lmax+1) B.
 template <int T>
 __global__ void __launch_bounds__(T) group_tables_kernel(const int32_t* H, int max_len, int W,
                                                          int c_stride, int s_stride, uint16_t* gC,
                                                          uint16_t* gS) {
-  __shared__ int scratch[64];
-  const int g = blockIdx.x;
+  extern __shared__ int cum[];  // [Lmax+1] inclusive prefix sums
+  __shared__ int scratch[T / 32];
+  const int g = blockIdx.x, split = blockIdx.y, n_split = gridDim.y;
   const int nb = max_len + 1;
   const int32_t* h = H + (int64_t)g * nb;
   uint16_t* C = gC + (int64_t)g * c_stride;
   uint16_t* S = gS + (int64_t)g * s_stride;
-  const int per = (nb + T - 1) / T;
-  const int lo = threadIdx.x * per, hi = min(nb, lo + per);
-  int s = 0;
-  for (int l = lo; l < hi; ++l) s += h[l];
-  int v[1] = {s}, tot[1];
-  block_exclusive_add<T, 1>(v, tot, scratch);
-  int acc = v[0];
-  for (int l = lo; l < hi; ++l) {
-    const int prev = acc;
-    acc += h[l];
-    C[l] = (uint16_t)min(acc, 65535);
-    for (int x = prev; x < acc && x < W; ++x) S[x] = (uint16_t)l;
+  int carry = 0;
+  for (int l0 = 0; l0 < nb; l0 += T) {
+    const int l = l0 + threadIdx.x;
+    int v[1] = {l < nb ? h[l] : 0}, tot[1];
+    const int own = v[0];
+    block_exclusive_add<T, 1>(v, tot, scratch);
+    const int inc = carry + v[0] + own;
+    if (l < nb) {
+      cum[l] = inc;
+      if (split == 0) C[l] = (uint16_t)min(inc, 65535);
+    }
+    carry += tot[0];
+  }
+  __syncthreads();
+  const int per = (W + n_split - 1) / n_split;
+  const int x0 = split * per, x1 = min(W, x0 + per);
+  for (int x = x0 + threadIdx.x; x < x1; x += T) {
+    int lo = 0, len = nb;  // first l with cum[l] > x
+    while (len > 0) {
+      const int half = len >> 1;
+      const bool right = cum[lo + half] <= x;
+      lo = right ? lo + half + 1 : lo;
+      len = right ? len - half - 1 : half;
+    }
+    S[x] = (uint16_t)lo;
   }
 }
 

@@ -5,8 +5,13 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
+
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums only; the functions are resolved with dlopen (nccl_api)
 
 #include "../../include/pfsched.h"
 #include "pf_admit.cuh"  // defines PF_BPT, PF_MINMAX, PF_LOCKSTEP_MAX
@@ -48,15 +53,22 @@ struct Variant {
   int TW, cap;       // team warps, max requests per instance served
   AdmitFn fn[3][3];  // [lookup][pack]
 };
-// pack index 0: unpacked; 1: A << 9 | N bins; 2: A << 10 | N bins (one-warp teams only)
+// pack index 0: unpacked; 1: A << 9 | N bins (requires max_entries < 512, so one-warp
+// teams only); 2: A << 10 | N bins (one-warp teams only). Variants that can never be
+// selected are not instantiated.
+template <int TW, int LOOK, int PK>
+AdmitFn packed_variant() {
+  if constexpr (TW == 1) return pf::admit_kernel<1, LOOK, PK>;
+  else return nullptr;
+}
 #define PF_VARIANT(TW, CAP)                                                                    \
   {TW, CAP,                                                                                   \
-   {{pf::admit_kernel<TW, pf::LOOK_SORTED, 0>, pf::admit_kernel<TW, pf::LOOK_SORTED, 9>,       \
-     TW == 1 ? pf::admit_kernel<TW, pf::LOOK_SORTED, 10> : nullptr},                          \
-    {pf::admit_kernel<TW, pf::LOOK_HIST, 0>, pf::admit_kernel<TW, pf::LOOK_HIST, 9>,           \
-     TW == 1 ? pf::admit_kernel<TW, pf::LOOK_HIST, 10> : nullptr},                            \
-    {pf::admit_kernel<TW, pf::LOOK_GROUP, 0>, pf::admit_kernel<TW, pf::LOOK_GROUP, 9>,         \
-     TW == 1 ? pf::admit_kernel<TW, pf::LOOK_GROUP, 10> : nullptr}}}
+   {{pf::admit_kernel<TW, pf::LOOK_SORTED, 0>, packed_variant<TW, pf::LOOK_SORTED, 9>(),       \
+     packed_variant<TW, pf::LOOK_SORTED, 10>()},                                              \
+    {pf::admit_kernel<TW, pf::LOOK_HIST, 0>, packed_variant<TW, pf::LOOK_HIST, 9>(),           \
+     packed_variant<TW, pf::LOOK_HIST, 10>()},                                                \
+    {pf::admit_kernel<TW, pf::LOOK_GROUP, 0>, packed_variant<TW, pf::LOOK_GROUP, 9>(),         \
+     packed_variant<TW, pf::LOOK_GROUP, 10>()}}}
 const Variant kVariants[] = {PF_VARIANT(1, 512), PF_VARIANT(2, 1024), PF_VARIANT(4, 2048),
                              PF_VARIANT(8, 4096)};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
@@ -105,9 +117,15 @@ struct pf_ctx {
   size_t admit_smem;   // per CTA
   int team_smem, ent_cap;
   int n_bins, bin_shift;
+  int teams;           // instance teams per CTA of the admit kernel
+  int carveout;        // preferred shared-memory carve-out (%) of the admit kernel, −1 = none
+  bool committed = false;  // group tables built at least once (shared mode)
+  void* comm = nullptr;    // ncclComm_t owned by the context (shared mode, nccl_unique_id set)
 };
 
 namespace {
+
+void nccl_destroy(void* comm);  // below
 
 void free_ctx(pf_ctx* c) {
   if (!c) return;
@@ -116,6 +134,7 @@ void free_ctx(pf_ctx* c) {
                   (void*)c->group_off, (void*)c->err, (void*)c->scratch,
                   (void*)c->edges})
     if (p) cudaFree(p);
+  if (c->comm) nccl_destroy(c->comm);
   delete c;
 }
 
@@ -134,14 +153,111 @@ int grid_for(int64_t total, int threads) {
   return (int)(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
 }
 
+// Kernel attributes are process-wide, but contexts of different sizes share kernel
+// variants: a context may only RAISE a kernel's dynamic shared-memory limit (a later,
+// smaller context must not lower it under an earlier one's launches), and the
+// carve-out hint is re-applied whenever the launching context's preference differs.
+std::mutex g_attr_mu;
+std::map<const void*, std::pair<int, int>> g_attr;  // fn -> (max dynamic smem set, carve-out %)
+
+cudaError_t ensure_smem(const void* fn, int bytes, int carveout_pct = -1) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_attr.find(fn);
+  if (it == g_attr.end()) it = g_attr.emplace(fn, std::make_pair(48 * 1024, -1)).first;
+  if (bytes > it->second.first) {
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    it->second.first = bytes;
+  }
+  if (carveout_pct >= 0 && carveout_pct != it->second.second) {
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct);
+    if (e != cudaSuccess) return e;
+    it->second.second = carveout_pct;
+  }
+  return cudaSuccess;
+}
+
+constexpr int kTablesThreads = 512;
+
 pf_status build_group_tables(pf_ctx* c, cudaStream_t s) {
   const int nxt = c->tbuf ^ 1;
   const size_t G = (size_t)c->cfg.n_groups;
-  pf::group_tables_kernel<256><<<c->cfg.n_groups, 256, 0, s>>>(
+  const int smem = (c->cfg.max_len + 1) * 4;
+  auto fn = pf::group_tables_kernel<kTablesThreads>;
+  PF_CUDA(ensure_smem(reinterpret_cast<const void*>(fn), smem));
+  // about two CTAs per SM in total: split each group's S_g fill over several CTAs
+  const int split = std::max(1, std::min(8, (2 * 148 + (int)G - 1) / (int)G));
+  fn<<<dim3((unsigned)G, (unsigned)split), kTablesThreads, smem, s>>>(
       c->xbuf, c->cfg.max_len, c->cfg.window, c->c_stride, c->s_stride,
       c->gC + nxt * G * c->c_stride, c->gS + nxt * G * c->s_stride);
   PF_CUDA(cudaGetLastError());
   c->tbuf = nxt;
+  c->committed = true;
+  return PF_OK;
+}
+
+// ---------------------------------------------------------------- NCCL (shared mode)
+// The context owns its communicator when the caller passes an ncclUniqueId
+// (pf_config.nccl_unique_id). NCCL is resolved at run time (dlopen "libnccl.so.2", or
+// $PFSCHED_NCCL_LIB): a process that already loaded NCCL (e.g. torch) shares that copy,
+// and contexts that never use NCCL do not need it.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::string why;
+};
+
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("PFSCHED_NCCL_LIB");
+    void* h = nullptr;
+    if (env && *env) {
+      h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    } else {
+      h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);  // already in the process
+      if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) {
+      api.why = std::string("cannot load NCCL: ") + dlerror();
+      return;
+    }
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy ||
+        !api.error_string)
+      api.why = "NCCL library lacks a required symbol";
+  });
+  return api.why.empty() ? &api : nullptr;
+}
+
+#define PF_NCCL(call)                                                                      \
+  do {                                                                                     \
+    const NcclApi* A_ = nccl_api();                                                        \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(PF_ENCCL, "%s: %s", #call, A_ ? A_->error_string(r_) : "NCCL unavailable"); \
+  } while (0)
+
+void nccl_destroy(void* comm) {
+  if (const NcclApi* A = nccl_api()) A->comm_destroy((ncclComm_t)comm);
+}
+
+// H_g = Σ_ranks (owned-shard histograms), in place in the exchange buffer, on `s`.
+pf_status exchange_in_library(pf_ctx* c, cudaStream_t s) {
+  const NcclApi* A = nccl_api();
+  if (!A) return fail(PF_ENCCL, "shared mode NCCL exchange: %s", "NCCL unavailable");
+  const size_t count = (size_t)c->cfg.n_groups * (c->cfg.max_len + 1);
+  PF_NCCL(A->all_reduce(c->xbuf, c->xbuf, count, ncclInt32, ncclSum, (ncclComm_t)c->comm, s));
   return PF_OK;
 }
 
@@ -152,6 +268,16 @@ extern "C" {
 int32_t pf_abi_version(void) { return PF_ABI_VERSION; }
 
 const char* pf_last_error(void) { return g_last_error.c_str(); }
+
+pf_status pf_nccl_unique_id(void* id_out) {
+  if (!id_out) return fail(PF_EINVAL, "pf_nccl_unique_id: NULL id_out");
+  const NcclApi* A = nccl_api();
+  if (!A) return fail(PF_ENCCL, "pf_nccl_unique_id: NCCL unavailable");
+  ncclUniqueId id;
+  PF_NCCL(A->get_unique_id(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return PF_OK;
+}
 
 pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* stream,
                     pf_ctx** out) {
@@ -179,10 +305,31 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   } else if (C.window > 16384 && C.window <= C.max_len + 1) {
     return fail(PF_ERANGE, "per-instance window <= Lmax+1 must be <= 16384");
   }
+  if (C.nccl_unique_id && C.n_groups == 0)
+    return fail(PF_EINVAL, "nccl_unique_id is only used in shared mode (n_groups > 0)");
   cudaStream_t s = S(stream);
   pf_ctx* c = new pf_ctx();
   c->cfg = C;
   c->cfg.group_off = nullptr;
+  c->cfg.nccl_unique_id = nullptr;  // not retained
+  if (C.nccl_unique_id) {
+    // context-owned communicator (collective: every rank calls pf_create with the same id)
+    const NcclApi* A = nccl_api();
+    if (!A) {
+      delete c;
+      return fail(PF_ENCCL, "pf_create: %s", "NCCL unavailable (dlopen libnccl.so.2 failed)");
+    }
+    ncclUniqueId id;
+    memcpy(&id, C.nccl_unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = A->comm_init_rank(&comm, C.nranks, id, C.rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return fail(PF_ENCCL, "pf_create: ncclCommInitRank(nranks=%d, rank=%d): %s", C.nranks, C.rank,
+                  A->error_string(r));
+    }
+    c->comm = comm;
+  }
   if (C.n_groups > 0) {
     c->layout = LAYOUT_GROUP;
     c->shards_owned = 8 / C.nranks;
@@ -190,6 +337,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     c->row_window = C.window / 8;
     c->rows_per_hist = c->shards_owned;
   } else {
+    c->committed = true;  // per-instance tables are built inside the admit kernel
     c->layout = (C.window <= C.max_len + 1) ? LAYOUT_SORTED : LAYOUT_HIST;
     c->shards_owned = 1;
     c->n_rows = C.n_instances;
@@ -222,8 +370,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     PF_CUDA_C(cudaMalloc(&c->sorted, ring_elems * 4 + 16));
     int P2 = 1;
     while (P2 < c->row_window) P2 <<= 1;
-    PF_CUDA_C(cudaFuncSetAttribute(pf::sort_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   P2 * 4));
+    PF_CUDA_C(ensure_smem(reinterpret_cast<const void*>(pf::sort_rows_kernel), P2 * 4));
     pf::sort_rows_kernel<<<c->n_rows, 512, P2 * 4, s>>>(c->ring, c->sorted, c->row_window, P2);
     PF_CUDA_C(cudaGetLastError());
   } else {
@@ -250,8 +397,9 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     dist_of_kernel<<<G, 128, 0, s>>>(c->group_off, G, C.n_instances, c->dist_of, c->scratch);
     PF_CUDA_C(cudaGetLastError());
     PF_CUDA_C(cudaMemcpyAsync(c->xbuf, c->hist, (size_t)G * nb * 4, cudaMemcpyDeviceToDevice, s));
-    if (C.nranks == 1) {
-      pf_status st = build_group_tables(c, s);
+    if (c->comm || C.nranks == 1) {
+      pf_status st = c->comm ? exchange_in_library(c, s) : PF_OK;
+      if (st == PF_OK) st = build_group_tables(c, s);
       if (st != PF_OK) return cleanup_fail(st);
     }
   }
@@ -302,31 +450,35 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
                 nbw * 8 + 140 * 4 + table;
   team = (team + 15) & ~(size_t)15;
   c->team_smem = (int)team;
-  c->admit_smem = team * teams_per_cta(V.TW);
+  // one-warp teams: PF_TEAMS1 per CTA, fewer when their shared memory does not fit
+  // (large per-instance histogram tables: Lmax up to 32767)
+  c->teams = teams_per_cta(V.TW);
+  while (c->teams > 1 && team * c->teams > 227 * 1024) --c->teams;
+  c->admit_smem = team * c->teams;
   const int look = c->layout;
   if (c->admit_smem > 227 * 1024) {
-    fail(PF_ERANGE, "admit kernel needs %zu B of shared memory", c->admit_smem);
+    fail(PF_ERANGE, "admit kernel needs %zu B of shared memory per instance team (> 227 KB)", c->admit_smem);
     return cleanup_fail(PF_ERANGE);
   }
-  PF_CUDA_C(cudaFuncSetAttribute(V.fn[look][c->pack], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)c->admit_smem));
+  const void* afn = reinterpret_cast<const void*>(V.fn[look][c->pack]);
+  PF_CUDA_C(ensure_smem(afn, (int)c->admit_smem));
 #ifndef PF_CARVEOUT
 #define PF_CARVEOUT 1
 #endif
+  c->carveout = -1;
   if (PF_CARVEOUT) {
     // Ask for the smallest shared-memory carve-out that keeps the full occupancy: the
     // rest of the 256 KB unified L1 caches the group tables (LOOK_GROUP lookups).
     int per_sm = 0;
     PF_CUDA_C(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, V.fn[look][c->pack], teams_per_cta(V.TW) * V.TW * 32, c->admit_smem));
+        &per_sm, V.fn[look][c->pack], c->teams * V.TW * 32, c->admit_smem));
     const size_t need = (size_t)std::max(1, per_sm) * (c->admit_smem + 1024);
     // the driver rounds the hint up to the next supported size (KiB)
     static const int kSizes[] = {0, 8, 16, 32, 64, 100, 132, 164, 196, 228};
     int kib = 228;
     for (int sz : kSizes)
       if ((size_t)sz * 1024 >= need) { kib = sz; break; }
-    const int pct = kib * 100 / 228;
-    PF_CUDA_C(cudaFuncSetAttribute(V.fn[look][c->pack], cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    c->carveout = kib * 100 / 228;
   }
 #undef PF_CUDA_C
   *out = c;
@@ -360,6 +512,11 @@ pf_status pf_update_history(pf_ctx* c, const int32_t* comp_off, const int32_t* c
   if (c->layout == LAYOUT_GROUP) {
     const size_t bytes = (size_t)c->cfg.n_groups * (c->cfg.max_len + 1) * 4;
     PF_CUDA(cudaMemcpyAsync(c->xbuf, c->hist, bytes, cudaMemcpyDeviceToDevice, s));
+    if (c->comm) {  // collective: H_g = Σ_ranks, then the tables, all on `s`
+      const pf_status st = exchange_in_library(c, s);
+      if (st != PF_OK) return st;
+      return build_group_tables(c, s);
+    }
     if (c->cfg.nranks == 1) return build_group_tables(c, s);
   }
   return PF_OK;
@@ -376,6 +533,9 @@ pf_status pf_exchange_buffer(pf_ctx* c, int32_t** buf, int64_t* count) {
 pf_status pf_commit_history(pf_ctx* c, void* stream) {
   if (!c) return fail(PF_EINVAL, "pf_commit_history: NULL ctx");
   if (c->layout != LAYOUT_GROUP) return PF_OK;
+  if (c->comm)
+    return fail(PF_ESTATE, "pf_commit_history: the context owns its NCCL communicator; "
+                           "pf_update_history already exchanged and rebuilt the tables");
   return build_group_tables(c, S(stream));
 }
 
@@ -387,6 +547,9 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
                               int32_t* pred_q_out, cudaStream_t s,
                               const int32_t* lhat_run = nullptr, const int32_t* lhat_q = nullptr) {
   const pf_config& C = c->cfg;
+  if (!c->committed)
+    return fail(PF_ESTATE, "shared mode with nranks > 1: all-reduce the exchange buffer and call "
+                           "pf_commit_history before the first admit / estimate");
   pf::AdmitParams p;
   memset(&p, 0, sizeof(p));
   p.n = C.n_instances;
@@ -433,8 +596,11 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.lhat_q = lhat_q;
   p.err = c->err;
   const Variant& V = kVariants[c->variant];
-  const int teams = teams_per_cta(V.TW);
+  const int teams = c->teams;
+  p.teams = teams;
   const int grid = (C.n_instances + teams - 1) / teams;
+  PF_CUDA(ensure_smem(reinterpret_cast<const void*>(V.fn[c->layout][c->pack]), (int)c->admit_smem,
+                      c->carveout));
   V.fn[c->layout][c->pack]<<<grid, teams * V.TW * 32, c->admit_smem, s>>>(p);
   PF_CUDA(cudaGetLastError());
   return PF_OK;
@@ -901,7 +1067,7 @@ pf_status pf_window_similarity(const int32_t* lengths, int64_t n, int32_t window
   if (!C && summary_out) PF_CUDA(cudaMallocAsync(&C, (size_t)B * B * 8, s));
   const size_t smem = (size_t)(max_len + 1) * 4;
   if (smem > 48 * 1024)
-    PF_CUDA(cudaFuncSetAttribute(pf::gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PF_CUDA(ensure_smem(reinterpret_cast<const void*>(pf::gram_kernel), (int)smem));
   pf::gram_kernel<<<B, 512, smem, s>>>(lengths, window, B, max_len, G);
   PF_CUDA(cudaGetLastError());
   if (C) {
@@ -930,7 +1096,7 @@ pf_status pf_adjacent_similarity(const int32_t* lengths, int64_t n, int32_t hist
   if (st != PF_OK) return st;
   const size_t smem = (size_t)2 * (max_len + 1) * 4;
   if (smem > 48 * 1024)
-    PF_CUDA(cudaFuncSetAttribute(pf::adjacent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PF_CUDA(ensure_smem(reinterpret_cast<const void*>(pf::adjacent_kernel), (int)smem));
   pf::adjacent_kernel<<<K, 512, smem, s>>>(lengths, hist_window, run_window, max_len, cos_out);
   if (mean_out) pf::mean_kernel<<<1, 1024, 0, s>>>(cos_out, K, mean_out);
   PF_CUDA(cudaGetLastError());
@@ -982,7 +1148,7 @@ pf_status pf_forward(pf_ctx* c, int32_t cluster_size, const int32_t* run_off,
   P.peak_out = peak_out;
   P.err = c->err;
   if (smem > 48 * 1024)
-    PF_CUDA(cudaFuncSetAttribute(pf::forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PF_CUDA(ensure_smem(reinterpret_cast<const void*>(pf::forward_kernel), (int)smem));
   pf::forward_kernel<<<P.n_clusters, cluster_size * 32, smem, S(stream)>>>(P);
   PF_CUDA(cudaGetLastError());
   return PF_OK;

@@ -33,14 +33,14 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.pf_abi_version() == 1
+    assert lib.pf_abi_version() == 2
 
 
 def _cfg(**kw):
     from paper_2507_10150_b200.binding import PFConfig
     base = dict(n_instances=4, window=100, max_len=512, max_input_len=512, max_entries=64, n_groups=0,
                 group_off=None, instance_base=0, members_per_group=0, member_base=0, mode=0,
-                quantile_u=0, repetitions=1, reserved_bp=0, seed=0, rank=0, nranks=1)
+                quantile_u=0, repetitions=1, reserved_bp=0, seed=0, rank=0, nranks=1, nccl_unique_id=None)
     base.update(kw)
     return PFConfig(**base)
 
@@ -51,6 +51,7 @@ def _cfg(**kw):
     (dict(mode=7), -1), (dict(max_input_len=10**7, max_entries=4096), -2),
     (dict(n_groups=2, window=100), -1), (dict(n_groups=2, window=96), -1),
     (dict(n_groups=2, window=96, group_off=1234, nranks=3), -1),
+    (dict(nccl_unique_id=1234), -1),  # a communicator only exists in shared mode
 ])
 def test_host_validation(lib, kw, status):
     h = ctypes.c_void_p()
@@ -103,3 +104,14 @@ def test_analysis_host_validation(lib):
 
 def test_forward_null_arguments(lib):
     assert lib.pf_forward(None, 1, *([None] * 7), 0, *([None] * 4)) == -1
+
+
+def test_nccl_unique_id(lib):
+    """pf_nccl_unique_id: NULL output is rejected; otherwise NCCL is dlopen'ed at run time
+    and writes 128 bytes (PF_ENCCL = -5 only if NCCL cannot be loaded)."""
+    assert lib.pf_nccl_unique_id(None) == -1
+    buf = ctypes.create_string_buffer(128)
+    st = lib.pf_nccl_unique_id(buf)
+    assert st in (0, -5), st
+    if st == 0:
+        assert any(buf.raw)

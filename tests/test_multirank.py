@@ -24,7 +24,7 @@ import oracle as O
 import workload as W
 from workload.gen import local_instance_ids, owned_shards
 
-CFG = W.scaled(W.CONFIGS[5], 64 * 4)  # 64 groups x 4 members
+CFG = W.scaled(W.CONFIGS[5], 64 * 8)  # 64 groups x 8 members (divisible by P = 8)
 TICKS = 2
 
 
@@ -108,7 +108,7 @@ def test_gloo_two_ranks_match_single_rank():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 def test_gpu_shared_mode_ranks_on_one_device(P):
     from paper_2507_10150_b200 import Scheduler
     b, orc, _ = _p1_reference()

@@ -200,6 +200,14 @@ class Batch:
     def slots(self) -> int:
         return int(self.run_off[-1]) + int(self.q_off[-1])
 
+    def clone(self) -> "Batch":
+        """Independent copies of every tensor (same values; e.g. L2 rotation in bench.py)."""
+        f = {}
+        for fld in dataclasses.fields(self):
+            v = getattr(self, fld.name)
+            f[fld.name] = v.clone() if isinstance(v, torch.Tensor) else v
+        return Batch(**f)
+
     def to(self, device) -> "Batch":
         f = {}
         for fld in dataclasses.fields(self):
