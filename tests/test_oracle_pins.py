@@ -432,3 +432,86 @@ def test_adaptive_repetitions_rule():
     for s, l_t in enumerate((0, 50)):
         umax = max(O.draw(K, s, 32, rep) for rep in range(32))
         assert out["pred_run"][s] == O.predict(win, l_t, 200, umax)
+
+
+# ---- C-8 / C-9 re-derived in pure Python (independent of the oracle's C++ hash) ----------
+_M64 = (1 << 64) - 1
+
+
+def _py_mix64(z):
+    z &= _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _py_lowbias32(x):
+    x &= 0xFFFFFFFF
+    x ^= x >> 16
+    x = (x * 0x7FEB352D) & 0xFFFFFFFF
+    x ^= x >> 15
+    x = (x * 0x846CA68B) & 0xFFFFFFFF
+    return x ^ (x >> 16)
+
+
+def _py_u(seed, tick, inst, slot, R):
+    """C-8: K = mix64(seed ^ tick·C_T ^ inst·C_I); u_rep = lowbias32(lo32 K ^ hi32 K ^
+    lo32((slot·R + rep)·0x9E3779B9)); C-9: u = max_rep u_rep (the inverse CDF is monotone)."""
+    K = _py_mix64(seed ^ ((tick * 0xD1B54A32D192ED03) & _M64) ^ ((inst * 0x9E3779B97F4A7C15) & _M64))
+    fold = (K & 0xFFFFFFFF) ^ (K >> 32)
+    return max(_py_lowbias32(fold ^ (((slot * R + rep) * 0x9E3779B9) & 0xFFFFFFFF)) for rep in range(R))
+
+
+def _py_predict(window, l_t, max_new, u):
+    gt = sorted(h for h in window if h > l_t)          # C-3/C-4: values > l_t, ascending
+    if not gt:
+        return max_new                                  # C-5
+    return min(gt[(u * len(gt)) >> 32], max_new)        # rank ⌊u·|gt|/2^32⌋, C-6
+
+
+def test_py_c8_pins_splitmix_vector():
+    # SplitMix64's published first output from state 0 (state += γ, then the finalizer)
+    assert _py_mix64(0x9E3779B97F4A7C15) == 0xE220A8397B1DCDAF
+
+
+@pytest.mark.parametrize("R", [2, 3, 7])
+def test_repetitions_gt1_against_pure_python(R):
+    """R > 1 draws (C-9 indexing (slot·R + rep)): every prediction of a small instance,
+    running and queued, equals the pure-Python re-derivation."""
+    rng = random.Random(R)
+    win = [rng.randint(1, 60) for _ in range(40)]
+    orc = O.Oracle(1, 40, 64, 1, np.array(win, dtype=np.int32)[None, :])
+    lp = [rng.randint(0, 50) for _ in range(5)]
+    lt = [rng.randint(0, 63) for _ in range(5)]
+    ql = [rng.randint(0, 50) for _ in range(4)]
+    seed, tick, inst = 0x1234567890ABCDEF, 7, 3
+    out = orc.admit(dist_of=[0], inst_id=[inst], run_off=[0, 5], input_len=lp, generated=lt, max_new=[64],
+                    q_off=[0, 4], q_input_len=ql, capacity=[10 ** 6], mode=0, repetitions=R, seed=seed,
+                    tick=tick, want_pred=True)
+    for s in range(5):
+        assert out["pred_run"][s] == _py_predict(win, lt[s], 64, _py_u(seed, tick, inst, s, R))
+    for j in range(4):  # queued slot k + j (0-based j), l_t = 0 (C-16)
+        assert out["pred_q"][j] == _py_predict(win, 0, 64, _py_u(seed, tick, inst, 5 + j, R))
+
+
+def test_adaptive_repetitions_at_k0_against_pure_python():
+    """Reading of SPEC.md:161's R = max(1, ⌈64/k⌉) at k = 0 (no running batch): R = 64 (the
+    k → 1 limit). Queued predictions of an instance with an empty running batch use 64 draws."""
+    rng = random.Random(99)
+    win = [rng.randint(1, 300) for _ in range(50)]
+    orc = O.Oracle(1, 50, 300, 1, np.array(win, dtype=np.int32)[None, :])
+    ql = [rng.randint(0, 100) for _ in range(6)]
+    seed, tick, inst = 42, 3, 11
+    out = orc.admit(dist_of=[0], inst_id=[inst], run_off=[0, 0], input_len=[], generated=[], max_new=[300],
+                    q_off=[0, 6], q_input_len=ql, capacity=[10 ** 6], mode=0, repetitions=0, seed=seed,
+                    tick=tick, want_pred=True)
+    for j in range(6):
+        assert out["pred_q"][j] == _py_predict(win, 0, 300, _py_u(seed, tick, inst, j, 64))
+    # and k = 3 gives R = ⌈64/3⌉ = 22
+    out = orc.admit(dist_of=[0], inst_id=[inst], run_off=[0, 3], input_len=[1, 2, 3], generated=[5, 0, 70],
+                    max_new=[300], q_off=[0, 2], q_input_len=ql[:2], capacity=[10 ** 6], mode=0,
+                    repetitions=0, seed=seed, tick=tick, want_pred=True)
+    for s, l_t in enumerate((5, 0, 70)):
+        assert out["pred_run"][s] == _py_predict(win, l_t, 300, _py_u(seed, tick, inst, s, 22))
+    for j in range(2):
+        assert out["pred_q"][j] == _py_predict(win, 0, 300, _py_u(seed, tick, inst, 3 + j, 22))

@@ -1,0 +1,49 @@
+#!/usr/bin/env bash
+# One parameterized driver for the GPU-box measurements (run under gpurun from the repo
+# root; everything it writes goes to gpurun_out/, which gpurun copies back).
+#
+#   bash tools/gpu.sh tests            pytest -m gpu + smoke()
+#   bash tools/gpu.sh bench [C...]      bench.py lines (default config 5, plus the given configs)
+#   bash tools/gpu.sh reference         bench.py --impl reference (the CPU oracle arm)
+#   bash tools/gpu.sh launches          ncu launch list (gpu__time_duration.sum) of a short bench run
+#   bash tools/gpu.sh ncu C TAG         ncu --set full of the config-C admit kernel -> gpurun_out/TAG.ncu-rep
+#   bash tools/gpu.sh ab "LIB..." "C..." A/B of libpfsched builds (PFSCHED_LIB) per config (tools/ab.sh)
+#   bash tools/gpu.sh parity [ARGS]     tests/full_parity.py (full-size, every instance vs the oracle)
+#   bash tools/gpu.sh ubench            tools/microbench/ubench (issue rates of the ops the kernel uses)
+#
+# Inputs: the in-tree libpfsched.so (built by __graft_entry__.build()), alternative builds
+# for `ab` passed as paths (e.g. tools/variants/*.so from build.build(extra=[...], out=...)).
+set -u
+mode=${1:-tests}
+shift || true
+mkdir -p gpurun_out
+case "$mode" in
+  tests)
+    timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest=$?"
+    tail -2 gpurun_out/pytest_gpu.txt
+    timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.txt 2>&1; echo "smoke=$?" ;;
+  bench)
+    timeout 400 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench=$?"
+    for c in "$@"; do
+      timeout 300 python bench.py --config "$c" --no-cpu-baseline > "gpurun_out/bench_cfg$c.json" 2> "gpurun_out/bench_cfg$c.err"
+      echo "cfg$c=$?"
+    done ;;
+  reference)
+    timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+    echo "reference=$?" ;;
+  launches)
+    timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
+      python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo "launches=$?" ;;
+  ncu)
+    c=${1:-5}; tag=${2:-admit_cfg$c}
+    timeout 600 ncu --set full --import-source on --clock-control none -k regex:admit_kernel -c 1 -o "gpurun_out/$tag" \
+      python tools/prof_admit.py --config "$c" --ticks 2 > "gpurun_out/$tag.log" 2>&1; echo "ncu=$?" ;;
+  ab)
+    bash tools/ab.sh "$1" "${2:-5}" ;;
+  parity)
+    timeout 3000 python tests/full_parity.py "$@" > gpurun_out/full_parity.log 2>&1; echo "parity=$?"
+    tail -12 gpurun_out/full_parity.log ;;
+  ubench)
+    ./tools/microbench/ubench > gpurun_out/ubench.txt 2>&1; echo "ubench=$?" ;;
+  *) echo "unknown mode $mode"; exit 2 ;;
+esac

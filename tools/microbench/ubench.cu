@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(1024) kern(unsigned seed, long long* cyc) {
       atomicAdd(&s[(w * 32 + lane) & 8191], x + i);
     } else if (MODE == 1) {     // ATOMS.ADD, pseudo-random bins in 512
       x = x * 1664525u + 1013904223u;
-      atomicAdd(&s[(w << 9) + (x >> 23)], x);
+      atomicAdd(&s[((w << 9) + (x >> 23)) & 8191], x);
     } else if (MODE == 2) {     // LDS, conflict-free
       acc += s[((i * 32) + lane + w * 32) & 8191];
     } else if (MODE == 3) {     // IADD3/LOP3 chain-free ALU work (4 independent ops)
