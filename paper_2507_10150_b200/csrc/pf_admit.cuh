@@ -41,10 +41,11 @@
 #endif
 // Track the smallest / largest r present in each bin (over all requests of the
 // instance) to tighten the bin bounds: lo_b = min r, hi_b = max r (exact T at the min;
-// bins holding one distinct r need no refinement). Pays off for multi-warp teams (large
-// instances); for one-warp teams the extra shared memory costs more L1 than it saves.
+// bins holding one distinct r need no refinement). Off: with the float-exponent bin map
+// few bins need refinement, and the two extra shared-memory atomics per request cost more
+// than they save (measured cfg 4: 0.857 -> 0.788 ms without them).
 #ifndef PF_MINMAX
-#define PF_MINMAX 1
+#define PF_MINMAX 0
 #endif
 // Prefetch of the instance's input streams at kernel entry: 1 = L1, 2 = L2, 0 = off.
 #ifndef PF_PREFETCH
@@ -95,7 +96,6 @@ struct AdmitParams {
   int team_smem;       // bytes of shared memory per team
   int teams;           // teams per CTA (one-warp teams: ≤ PF_TEAMS1, fewer for large tables)
   int ent_cap;         // request slots per team (>= max_entries)
-  int bin_shift;            // s of the r -> bin map (bin_of)
   const uint32_t* edges;   // [n_bins]: lo | hi << 16 (0 = no r maps to the bin)
   // history tables
   const int32_t* sorted;     // LOOK_SORTED [n × w]
@@ -103,7 +103,7 @@ struct AdmitParams {
   const uint16_t* gC;        // LOOK_GROUP  [G × c_stride]: C_g[l] = #{h ≤ l} (u16, W < 2^16)
   const uint16_t* gS;        // LOOK_GROUP  [G × s_stride]: sorted group window (u16)
   int c_stride, s_stride;    // row strides (multiples of 8 elements)
-  int csh;                   // LOOK_SORTED: coarse-index bucket width 2^csh (64 buckets)
+  int cbits;                 // LOOK_SORTED: log2 of the coarse-index bucket count
   const int32_t* dist_of;    // LOOK_GROUP  [n]
   const int32_t* group_off;  // LOOK_GROUP  [G+1]
   // inputs
@@ -127,16 +127,23 @@ struct AdmitParams {
   const int32_t* lhat_q;     // [q_off[n]]
 };
 
-// r -> bin (r ≥ 1), the log-linear map of DESIGN.md §5 computed in registers: f(r) = r − 1
-// for r ≤ 2^(KO+1) (exact bins), else 2^KO·sh + (r >> sh) with sh = min(⌊log2 r⌋ − KO, s)
-// (2^KO bins per octave, then width 2^s); bins are stored descending, b = NB − 1 − f(r).
-// The host builds the per-bin edges from the same map (pfsched.cu bin_f).
+// r -> bin (r ≥ 1), stored descending: b = NB − 1 − f(r), f monotone non-decreasing:
+// the float-exponent map f(r) = bits(float(r)) >> (23 − SUB) − bits(1.0f) >> (23 − SUB)
+// with 2^SUB = NB/16 sub-bins per octave (one I2F, one shift, one add). Every r ≤ 2^SUB
+// has its own bin and Lmax ≤ 32767 needs < 15·2^SUB < NB bins. The bins stay logarithmic
+// all the way up (width ∝ r), which keeps the slack (hi − lo)·N of the bin bounds small
+// where the maximum sits: fewer bins need exact refinement than with the round-1
+// log-linear map (cfg 4: 0.41 vs 1.94 candidate bins per evaluation). The host builds the
+// per-bin edges from the same map (pfsched.cu bin_f).
 template <int NB>
-__device__ __forceinline__ int bin_of(int r, int s) {
-  constexpr int KO = (PF_BPT == 2) ? 2 : (PF_BPT == 4) ? 3 : 4;
-  const int sh = ::min(31 - KO - __clz(r), s);
-  const int f = r <= (2 << KO) ? r - 1 : (sh << KO) + (r >> sh);
-  return NB - 1 - f;
+constexpr int flog_sub() {
+  return NB == 128 ? 3 : NB == 256 ? 4 : NB == 512 ? 5 : NB == 1024 ? 6 : 7;
+}
+template <int NB>
+__device__ __forceinline__ int bin_of(int r) {
+  constexpr int SUB = flog_sub<NB>();
+  const unsigned fb = __float_as_uint(__uint2float_rz((unsigned)r)) >> (23 - SUB);  // exact: r < 2^24
+  return (NB - 1 + (127 << SUB)) - (int)fb;
 }
 
 // L1 prefetch of the 128-byte lines covering x[0..n), one line per thread per pass.
@@ -326,7 +333,7 @@ struct Eval {
 //   binR[NBW] u32, binQ[NBW] u32: per-bin (A, N) — packed A << 9 | N when PACK, else
 //                    A in [0, NB) and N in [NB, 2·NB)
 //   xs[140] i32      scratch: reductions [0,32), pick [32,34), list size [36], candidates [40,137)
-//   table            S[w+1] u16 + coarse index cidx[66] i32 (LOOK_SORTED) | C[Lmax+1] i32 (LOOK_HIST)
+//   table            S[w+1] u16 + coarse index cidx[2^cbits + 2] u16 (LOOK_SORTED) | C[Lmax+1] i32 (LOOK_HIST)
 // (the per-bin r ranges `edges` are read through L1 from global memory: 512 B per launch)
 template <int TW, int LOOK, int PK>
 // Resident 4-team CTAs per SM for one-warp teams (register cap 65536 / (128 · PF_MIN_CTAS)):
@@ -339,10 +346,11 @@ template <int TW, int LOOK, int PK>
 #define PF_TEAMS1 4
 #endif
 // Multi-warp teams (one team per CTA): resident warps per SM the register cap aims at
-// (min CTAs = PF_MW_WARPS / TW). cfg4 (TW = 4): 28 → 7 CTAs, 73 registers; measured
+// (min CTAs = PF_MW_WARPS / TW). cfg4 (TW = 4): 32 → 8 CTAs, 64 registers (round 2: −4 %
+// against 28 → 7 CTAs, 72 registers, once the per-bin min/max atomics were gone); measured
 // 2 CTAs (the old bound, ~110 registers, 4-5 resident) 1.29 ms → 8 CTAs 0.96 ms.
 #ifndef PF_MW_WARPS
-#define PF_MW_WARPS 28
+#define PF_MW_WARPS 32
 #endif
 #if PF_LOCKSTEP_MAX > 16
 #error "PF_LOCKSTEP_MAX > 16 overflows the candidate table"
@@ -455,22 +463,22 @@ admit_kernel(AdmitParams p) {
       }
     }
   }
-  // LOOK_SORTED coarse index over the sorted window: cidx[c] = #{S < c·2^csh}, c ≤ 64,
-  // so upper_bound(S, l) is a binary search inside [cidx[l >> csh], cidx[(l >> csh) + 1]).
-  int* cidx = table + ((w + 2) >> 1);  // after tS[0..w]; tS[w] = sentinel above every l̂ (n_gt = 0 → max_new)
-  int csh = 0;  // smallest s with (Lmax+1) >> s ≤ 64
-  if constexpr (TW > 1) {
-    csh = p.csh;  // (host)
-  } else {
-    while (((p.max_len + 1) >> csh) > 64) ++csh;
-  }
+  // LOOK_SORTED coarse index over the sorted window: cidx[c] = #{S < c·2^csh} for
+  // c ∈ [0, NCB + 1] (NCB = 2^cbits buckets, host-chosen), so upper_bound(S, l) is a
+  // binary search inside [cidx[l >> csh], cidx[(l >> csh) + 1]).
+  // Built with one lower_bound per bucket edge (a scatter build from the sorted window —
+  // entry x writes the buckets it opens — was measured slower: cfg 3 +26 %, cfg 4 +6 %).
+  uint16_t* cidx = reinterpret_cast<uint16_t*>(table) + ((w + 2) & ~1);  // after tS[0..w] (tS[w] = sentinel)
+  const int ncb = 1 << p.cbits;
+  int csh = 0;  // smallest s with (Lmax+1) >> s ≤ NCB
+  while (((p.max_len + 1) >> csh) > ncb) ++csh;
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
     for (int x = tid; x < w; x += TT) tS[x] = (uint16_t)__ldg(src + x);
     if (tid == 0) tS[w] = 0xFFFF;
     T.sync();
-    for (int c = tid; c <= 65; c += TT) {
-      const int v = c << csh;  // lower_bound(S, v)
+    for (int c = tid; c <= ncb + 1; c += TT) {  // one lower_bound per bucket edge
+      const int v = c << csh;
       int lo = 0, len = w;
       while (len > 0) {
         const int half = len >> 1;
@@ -478,7 +486,7 @@ admit_kernel(AdmitParams p) {
         lo = right ? lo + half + 1 : lo;
         len = right ? len - half - 1 : half;
       }
-      cidx[c] = (c == 65) ? w : lo;
+      cidx[c] = (uint16_t)lo;
     }
   } else if (LOOK == LOOK_HIST) {
     // C[l] = #{h ∈ L_h : h ≤ l}: inclusive scan of the persistent histogram.
@@ -521,7 +529,7 @@ admit_kernel(AdmitParams p) {
   auto finish = [&](int e, int l_hat, int l_t, int l_p, bool run) {
     const int r = l_hat - l_t;  // ≥ 1 (C-4)
     const int a = l_p + l_t;
-    const int b = bin_of<NB>(r, p.bin_shift);
+    const int b = bin_of<NB>(r);
     if (PACK) {
       rb[e] = (uint32_t)r | ((uint32_t)a << 13);
     } else {
@@ -1014,7 +1022,7 @@ admit_kernel(AdmitParams p) {
     }
     T.sync();
     for (int jx = tid; jx < ph; jx += TT) {
-      const int b = PACK ? bin_of<NB>(ent_r(k + jx), p.bin_shift) : (int)(rb[k + jx] >> 16);
+      const int b = PACK ? bin_of<NB>(ent_r(k + jx)) : (int)(rb[k + jx] >> 16);
       const int a = ent_a(k + jx);
       if (PACK) {
         atomicAdd(&binQ[b], ((uint32_t)a << NSH) | 1u);

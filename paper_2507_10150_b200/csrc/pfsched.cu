@@ -21,6 +21,14 @@
 #include "pf_analysis.cuh"
 #include "pf_forward.cuh"
 
+// LOOK_SORTED coarse-index size (log2 buckets) for multi-warp / one-warp teams.
+#ifndef PF_CIDX_BITS_MW
+#define PF_CIDX_BITS_MW 6
+#endif
+#ifndef PF_CIDX_BITS_1
+#define PF_CIDX_BITS_1 6
+#endif
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -74,20 +82,15 @@ const Variant kVariants[] = {PF_VARIANT(1, 512), PF_VARIANT(2, 1024), PF_VARIANT
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 inline int teams_per_cta(int TW) { return TW == 1 ? PF_TEAMS1 : 1; }
 
-// Host copy of the kernel's log-linear bin map f(r) (pf_admit.cuh header), with
-// 2^KO sub-bins per octave (KO = log2(4·PF_BPT/2)): width-1 bins for r ≤ 2^(KO+1),
-// 2^KO bins per octave up to width 2^s, then width 2^s.
-int bin_f(int r, int s) {
-  const int KO = (PF_BPT == 2) ? 2 : (PF_BPT == 4) ? 3 : 4;
-  const int E = 2 << KO;
-  if (r <= E) return r - 1;
-  const int r0 = 1 << (s + KO);
-  if (r < r0) {
-    int o = 0;
-    while ((2 << o) <= r) ++o;
-    return E + (1 << KO) * (o - KO - 1) + ((r - (1 << o)) >> (o - KO));
-  }
-  return E + (1 << KO) * (s - 1) + ((r - r0) >> s);
+// Host copy of the kernel's r -> bin map f(r) (pf_admit.cuh bin_of): the float exponent
+// and top SUB mantissa bits of r, 2^SUB = n_bins / 16 sub-bins per octave.
+int bin_f(int r, int n_bins) {
+  int sub = 0;
+  while ((16 << sub) < n_bins) ++sub;
+  const float fr = (float)r;
+  uint32_t bits;
+  memcpy(&bits, &fr, 4);
+  return (int)(bits >> (23 - sub)) - (127 << sub);
 }
 
 }  // namespace
@@ -116,7 +119,8 @@ struct pf_ctx {
   int variant;
   size_t admit_smem;   // per CTA
   int team_smem, ent_cap;
-  int n_bins, bin_shift;
+  int n_bins;
+  int cbits;           // LOOK_SORTED coarse index: 2^cbits buckets
   int teams;           // instance teams per CTA of the admit kernel
   int carveout;        // preferred shared-memory carve-out (%) of the admit kernel, −1 = none
   bool committed = false;  // group tables built at least once (shared mode)
@@ -416,12 +420,10 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     if (kVariants[v].cap >= C.max_entries) { c->variant = v; break; }
   const Variant& V = kVariants[c->variant];
   c->n_bins = 32 * PF_BPT * V.TW;
-  c->bin_shift = 1;
-  while (bin_f(C.max_len, c->bin_shift) > c->n_bins - 1) ++c->bin_shift;
   {  // per-bin r ranges of the r -> bin map (the kernel computes the map: bin_of)
     std::vector<uint32_t> ed(c->n_bins, 0);
     for (int r = 1; r <= C.max_len; ++r) {
-      const int b = c->n_bins - 1 - bin_f(r, c->bin_shift);
+      const int b = c->n_bins - 1 - bin_f(r, c->n_bins);
       const uint32_t lo = ed[b] ? (ed[b] & 0xFFFF) : (uint32_t)r;
       ed[b] = lo | ((uint32_t)r << 16);
     }
@@ -442,7 +444,11 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
       c->pack = 0;
   }
   size_t table = 0;
-  if (c->layout == LAYOUT_SORTED) table = (size_t)((C.window + 2) >> 1) * 4 + 66 * 4;  // u16 S + sentinel, coarse index
+  // LOOK_SORTED coarse index: 2^cbits buckets (64: finer indexes cost more to build than
+  // their shorter searches save, measured cfg 4: 256 buckets +3 %, 512 +9 %)
+  c->cbits = V.TW > 1 ? PF_CIDX_BITS_MW : PF_CIDX_BITS_1;
+  if (c->layout == LAYOUT_SORTED)
+    table = (size_t)((C.window + 2) & ~1) * 2 + (size_t)((1 << c->cbits) + 2) * 2;  // u16 S + sentinel, u16 index
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
   c->ent_cap = (C.max_entries + 7) & ~7;
   const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
@@ -566,7 +572,6 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.instance_base = C.instance_base;
   p.members_per_group = C.members_per_group;
   p.member_base = C.member_base;
-  p.bin_shift = c->bin_shift;
   p.edges = c->edges;
   p.team_smem = c->team_smem;
   p.ent_cap = c->ent_cap;
@@ -575,8 +580,7 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.gC = c->gC ? c->gC + (size_t)c->tbuf * C.n_groups * c->c_stride : nullptr;
   p.gS = c->gS ? c->gS + (size_t)c->tbuf * C.n_groups * c->s_stride : nullptr;
   p.c_stride = c->c_stride;
-  p.csh = 0;
-  while (((C.max_len + 1) >> p.csh) > 64) ++p.csh;
+  p.cbits = c->cbits;
   p.s_stride = c->s_stride;
   p.dist_of = c->dist_of;
   p.group_off = c->group_off;
