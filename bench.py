@@ -439,7 +439,17 @@ def main():
     peak_gbs, peak_src = peaks()
     abytes = algorithmic_bytes(cfg, bd)
     achieved = abytes / (kern_ms * 1e-3) / 1e9
-    traffic, traffic_src = measured_traffic(args.config, world, args.weak)
+    traffic, traffic_src, inst = measured_traffic(args.config, world, args.weak)
+    issue = None
+    if inst and clk.get("sm_mhz"):
+        # issue roofline next to the HBM one: the kernel's measured warp-instructions (ncu) per
+        # launch ÷ its live launch time vs 4 warp-instructions per SM-cycle × SMs × SM clock
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        peak_wi = 4 * sms * clk["sm_mhz"] * 1e6
+        ach_wi = inst / (kern_ms * 1e-3)
+        issue = {"achieved": ach_wi / 1e12, "peak": peak_wi / 1e12, "unit": "Twarp-instr/s",
+                 "frac": ach_wi / peak_wi, "warp_instructions_per_launch": inst,
+                 "per_instance": inst / n, "source": traffic_src}
 
     # e2e through the public API with HOST buffers (pinned), copies inside the timed region
     host = {k: getattr(bd, k).cpu().pin_memory() for k in
@@ -550,7 +560,7 @@ def main():
                          "frac": achieved / peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": abytes, "kernel": "admit_kernel",
-                         "frac_of_8TBs_spec": achieved / 8000.0},
+                         "frac_of_8TBs_spec": achieved / 8000.0, "issue": issue},
             "e2e": {"value": e2e_value, "unit": UNIT, "pipelined": "step t+1's H2D overlaps step t",
                     "h2d_bytes_per_step": int(h2d + h2d_c),
                     "d2h_bytes_per_step": int(d2h)},
@@ -569,15 +579,15 @@ def measured_traffic(config, world, weak):
     """ncu dram__bytes_read.sum + dram__bytes_write.sum per admit launch, from the ncu
     --set full capture of this config at N = 1 (profiles/admit_traffic.json), else None."""
     if world > 1 and not weak:
-        return None, "not captured for a 1/N shard"
+        return None, "not captured for a 1/N shard", None
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "admit_traffic.json")))
         e = d.get(f"cfg{config}")
         if isinstance(e, dict):
-            return e.get("bytes"), e.get("source")
+            return e.get("bytes"), e.get("source"), e.get("warp_instructions")
     except Exception:
         pass
-    return None, "no ncu capture for this config"
+    return None, "no ncu capture for this config", None
 
 
 def run_latency(args, rank, world, local):
