@@ -104,6 +104,7 @@ struct AdmitParams {
   const uint16_t* gS;        // LOOK_GROUP  [G × s_stride]: sorted group window (u16)
   int c_stride, s_stride;    // row strides (multiples of 8 elements)
   int cbits;                 // LOOK_SORTED: log2 of the coarse-index bucket count
+  int csh;                   // LOOK_SORTED: bucket width 2^csh, smallest with (Lmax+1) >> csh ≤ 2^cbits
   const int32_t* dist_of;    // LOOK_GROUP  [n]
   const int32_t* group_off;  // LOOK_GROUP  [G+1]
   // inputs
@@ -470,8 +471,7 @@ admit_kernel(AdmitParams p) {
   // entry x writes the buckets it opens — was measured slower: cfg 3 +26 %, cfg 4 +6 %).
   uint16_t* cidx = reinterpret_cast<uint16_t*>(table) + ((w + 2) & ~1);  // after tS[0..w] (tS[w] = sentinel)
   const int ncb = 1 << p.cbits;
-  int csh = 0;  // smallest s with (Lmax+1) >> s ≤ NCB
-  while (((p.max_len + 1) >> csh) > ncb) ++csh;
+  const int csh = p.csh;  // (host)
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
     for (int x = tid; x < w; x += TT) tS[x] = (uint16_t)__ldg(src + x);

@@ -581,6 +581,8 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.gS = c->gS ? c->gS + (size_t)c->tbuf * C.n_groups * c->s_stride : nullptr;
   p.c_stride = c->c_stride;
   p.cbits = c->cbits;
+  p.csh = 0;
+  while (((C.max_len + 1) >> p.csh) > (1 << c->cbits)) ++p.csh;
   p.s_stride = c->s_stride;
   p.dist_of = c->dist_of;
   p.group_off = c->group_off;
