@@ -79,31 +79,84 @@ __device__ __forceinline__ bool row_valid(const int32_t* comp_len, int c0, int c
   return !__any_sync(0xffffffffu, bad);
 }
 
-// #{x < v} and #{x ≤ v} over ascending global row S[0..w).
-__device__ __forceinline__ int lower_bound_g(const int32_t* S, int w, int v) {
-  int lo = 0, len = w;
-  while (len > 0) {
-    int half = len >> 1;
-    bool right = S[lo + half] < v;
-    lo = right ? lo + half + 1 : lo;
-    len = right ? len - half - 1 : half;
+// Warp-cooperative rank queries on an ascending global row S[0..w): #{x : S[x] < v}
+// (upper = false) and #{x : S[x] ≤ v} (upper = true) for two values at once. Each round
+// splits the candidate range into 32 segments and reads one pivot per lane (one memory
+// round trip for both queries); S sorted makes the predicate a prefix of the lanes, so
+// popc(ballot) picks the segment. w ≤ 1024: two rounds (round 1 used 10 dependent loads
+// per binary search).
+__device__ __forceinline__ void warp_rank2(const int32_t* S, int w, int va, bool ua, int vb, bool ub,
+                                           int lane, int& ra, int& rb) {
+  int lo_a = 0, hi_a = w, lo_b = 0, hi_b = w;
+  while (hi_a - lo_a > 0 || hi_b - lo_b > 0) {
+    const int na = hi_a - lo_a, nb = hi_b - lo_b;
+    const int sa = (na + 31) >> 5, sb = (nb + 31) >> 5;  // segment lengths (≥ 1 when n > 0)
+    // pivot of lane l: last element of segment l (if the segment is non-empty)
+    const int pa = lo_a + (lane + 1) * sa - 1, pb = lo_b + (lane + 1) * sb - 1;
+    const bool oka = na > 0 && pa < hi_a, okb = nb > 0 && pb < hi_b;
+    const int xa = oka ? S[pa] : 0, xb = okb ? S[pb] : 0;
+    const unsigned ma = __ballot_sync(0xffffffffu, oka && (ua ? xa <= va : xa < va));
+    const unsigned mb = __ballot_sync(0xffffffffu, okb && (ub ? xb <= vb : xb < vb));
+    if (na > 0) {  // segments fully counted: popc(ma); the answer lies in the next segment
+      const int c = __popc(ma);
+      if (sa == 1) { lo_a += c; hi_a = lo_a; }
+      else { lo_a += c * sa; hi_a = ::min(hi_a, lo_a + sa - 1); }  // its last element failed
+    }
+    if (nb > 0) {
+      const int c = __popc(mb);
+      if (sb == 1) { lo_b += c; hi_b = lo_b; }
+      else { lo_b += c * sb; hi_b = ::min(hi_b, lo_b + sb - 1); }
+    }
   }
-  return lo;
+  ra = lo_a;
+  rb = lo_b;
 }
-__device__ __forceinline__ int upper_bound_g(const int32_t* S, int w, int v) {
-  int lo = 0, len = w;
-  while (len > 0) {
-    int half = len >> 1;
-    bool right = S[lo + half] <= v;
-    lo = right ? lo + half + 1 : lo;
-    len = right ? len - half - 1 : half;
+
+// Move S[src .. src + n) to S[dst .. dst + n) with dst = src ∓ 1 (one-slot shift), in
+// batches of 8 elements per lane (loads of a batch in flight together). Ascending order
+// when dst < src, descending when dst > src, so no batch reads a slot already written.
+__device__ __forceinline__ void warp_shift1(int32_t* S, int src, int dst, int n, int lane) {
+  constexpr int B = 8 * 32;
+  if (dst < src) {
+    for (int b0 = 0; b0 < n; b0 += B) {
+      int v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int x = b0 + t * 32 + lane;
+        v[t] = x < n ? S[src + x] : 0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int x = b0 + t * 32 + lane;
+        if (x < n) S[dst + x] = v[t];
+      }
+      __syncwarp();
+    }
+  } else {
+    for (int b0 = 0; b0 < n; b0 += B) {
+      int v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int x = n - 1 - (b0 + t * 32 + lane);
+        v[t] = x >= 0 ? S[src + x] : 0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int x = n - 1 - (b0 + t * 32 + lane);
+        if (x >= 0) S[dst + x] = v[t];
+      }
+      __syncwarp();
+    }
   }
-  return lo;
 }
 
 // Per-instance rings with a maintained sorted copy (w ≤ Lmax+1). Warp per row;
 // completions applied one at a time in order: evict v_old = ring[head], append
-// v_new, and move the sorted copy's elements between the two positions by one.
+// v_new, and move the sorted copy's elements between the two positions by one
+// (warp-cooperative rank queries + batched shift: a few memory round trips per
+// completion instead of two 10-step dependent binary searches).
 __global__ void update_sorted_kernel(int n_rows, int w, int max_len, const int32_t* comp_off,
                                      const int32_t* comp_len, int32_t* ring, int32_t* head,
                                      int32_t* sorted, int* err) {
@@ -127,28 +180,18 @@ __global__ void update_sorted_kernel(int n_rows, int w, int max_len, const int32
     h = (h + 1 == w) ? 0 : h + 1;
     if (v_new == v_old) continue;
     if (v_new > v_old) {
-      // remove first v_old at i, insert v_new at j: S[i..j-1] <- S[i+1..j], S[j] = v_new
-      const int i = lower_bound_g(S, w, v_old);
-      const int j = upper_bound_g(S, w, v_new) - 1;
-      for (int x0 = i; x0 < j; x0 += 32) {
-        const int x = x0 + lane;
-        const int v = (x < j) ? S[x + 1] : 0;
-        __syncwarp();
-        if (x < j) S[x] = v;
-        __syncwarp();
-      }
+      // remove the first v_old (at i), insert v_new at j: S[i..j-1] <- S[i+1..j], S[j] = v_new
+      int i, j1;
+      warp_rank2(S, w, v_old, false, v_new, true, lane, i, j1);
+      const int j = j1 - 1;
+      warp_shift1(S, i + 1, i, j - i, lane);
       if (lane == 0) S[j] = v_new;
     } else {
-      // remove last v_old at i, insert v_new at j: S[j+1..i] <- S[j..i-1], S[j] = v_new
-      const int i = upper_bound_g(S, w, v_old) - 1;
-      const int j = upper_bound_g(S, w, v_new);
-      for (int x1 = i; x1 > j; x1 -= 32) {
-        const int x = x1 - lane;
-        const int v = (x > j) ? S[x - 1] : 0;
-        __syncwarp();
-        if (x > j) S[x] = v;
-        __syncwarp();
-      }
+      // remove the last v_old (at i), insert v_new at j: S[j+1..i] <- S[j..i-1], S[j] = v_new
+      int i1, j;
+      warp_rank2(S, w, v_old, true, v_new, true, lane, i1, j);
+      const int i = i1 - 1;
+      warp_shift1(S, j, j + 1, i - j, lane);
       if (lane == 0) S[j] = v_new;
     }
     __syncwarp();
@@ -198,7 +241,8 @@ __global__ void update_hist_kernel(int n_rows, int row_window, int rows_per_hist
 // Group tables from the (all-reduced) group histogram H_g: C_g[l] = Σ_{l'≤l} H_g[l']
 // and the sorted window S_g (S_g[x] = min{l : C_g[l] > x}), both u16 (W < 2^16,
 // Lmax < 2^15) with row strides c_stride / s_stride. Grid (G, SPLIT): every CTA of a
-// group scans the group's histogram into shared memory (coalesced, T per pass); split 0
+// group scans the group's histogram into shared memory (each thread a contiguous run,
+// loaded in one round trip, one block scan); split 0
 // stores C_g; split z fills S_g[x] for its x-range by a binary search in the shared copy
 // (one independent search per entry, no serial per-bin loops). Shared memory: 4·(Lmax+1) B.
 template <int T>
@@ -212,22 +256,34 @@ __global__ void __launch_bounds__(T) group_tables_kernel(const int32_t* H, int m
   const int32_t* h = H + (int64_t)g * nb;
   uint16_t* C = gC + (int64_t)g * c_stride;
   uint16_t* S = gS + (int64_t)g * s_stride;
-  int carry = 0;
-  for (int l0 = 0; l0 < nb; l0 += T) {
-    const int l = l0 + threadIdx.x;
-    int v[1] = {l < nb ? h[l] : 0}, tot[1];
-    const int own = v[0];
-    block_exclusive_add<T, 1>(v, tot, scratch);
-    const int inc = carry + v[0] + own;
-    if (l < nb) {
-      cum[l] = inc;
-      if (split == 0) C[l] = (uint16_t)min(inc, 65535);
+  // thread t owns the contiguous run [t·per, t·per + per): all its loads are issued at once
+  // (one memory round trip), then one block scan of the run sums
+  constexpr int MAXPER = 64;  // Lmax + 1 ≤ 32768 = 512 · 64
+  const int per = (nb + T - 1) / T;
+  const int l0 = threadIdx.x * per;
+  int v[MAXPER];
+  int sum = 0;
+#pragma unroll
+  for (int x = 0; x < MAXPER; ++x) {
+    if (x < per) {
+      v[x] = (l0 + x < nb) ? h[l0 + x] : 0;
+      sum += v[x];
     }
-    carry += tot[0];
+  }
+  int sv[1] = {sum}, tot[1];
+  block_exclusive_add<T, 1>(sv, tot, scratch);
+  int acc = sv[0];
+#pragma unroll
+  for (int x = 0; x < MAXPER; ++x) {
+    if (x < per && l0 + x < nb) {
+      acc += v[x];
+      cum[l0 + x] = acc;
+      if (split == 0) C[l0 + x] = (uint16_t)min(acc, 65535);
+    }
   }
   __syncthreads();
-  const int per = (W + n_split - 1) / n_split;
-  const int x0 = split * per, x1 = min(W, x0 + per);
+  const int sper = (W + n_split - 1) / n_split;
+  const int x0 = split * sper, x1 = min(W, x0 + sper);
   for (int x = x0 + threadIdx.x; x < x1; x += T) {
     int lo = 0, len = nb;  // first l with cum[l] > x
     while (len > 0) {

@@ -189,8 +189,11 @@ pf_status build_group_tables(pf_ctx* c, cudaStream_t s) {
   const int smem = (c->cfg.max_len + 1) * 4;
   auto fn = pf::group_tables_kernel<kTablesThreads>;
   PF_CUDA(ensure_smem(reinterpret_cast<const void*>(fn), smem));
-  // about two CTAs per SM in total: split each group's S_g fill over several CTAs
-  const int split = std::max(1, std::min(8, (2 * 148 + (int)G - 1) / (int)G));
+  // one wave (one 512-thread CTA per SM): split each group's S_g fill over several CTAs
+  int dev = 0, sms = 148;
+  PF_CUDA(cudaGetDevice(&dev));
+  PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int split = std::max(1, std::min(8, sms / (int)G));
   fn<<<dim3((unsigned)G, (unsigned)split), kTablesThreads, smem, s>>>(
       c->xbuf, c->cfg.max_len, c->cfg.window, c->c_stride, c->s_stride,
       c->gC + nxt * G * c->c_stride, c->gS + nxt * G * c->s_stride);
