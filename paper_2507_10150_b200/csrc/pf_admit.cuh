@@ -474,7 +474,16 @@ admit_kernel(AdmitParams p) {
   const int csh = p.csh;  // (host)
   if (LOOK == LOOK_SORTED) {
     const int32_t* src = p.sorted + (int64_t)i * w;
-    for (int x = tid; x < w; x += TT) tS[x] = (uint16_t)__ldg(src + x);
+    if ((w & 3) == 0) {  // rows are 16-byte aligned: 4 values per load, two packed u16 pairs per store
+      const int4* src4 = reinterpret_cast<const int4*>(src);
+      uint2* dst = reinterpret_cast<uint2*>(tS);
+      for (int x = tid; x < (w >> 2); x += TT) {
+        const int4 v = __ldg(src4 + x);
+        dst[x] = make_uint2((uint32_t)v.x | ((uint32_t)v.y << 16), (uint32_t)v.z | ((uint32_t)v.w << 16));
+      }
+    } else {
+      for (int x = tid; x < w; x += TT) tS[x] = (uint16_t)__ldg(src + x);
+    }
     if (tid == 0) tS[w] = 0xFFFF;
     T.sync();
     for (int c = tid; c <= ncb + 1; c += TT) {  // one lower_bound per bucket edge
@@ -489,18 +498,28 @@ admit_kernel(AdmitParams p) {
       cidx[c] = (uint16_t)lo;
     }
   } else if (LOOK == LOOK_HIST) {
-    // C[l] = #{h ∈ L_h : h ≤ l}: inclusive scan of the persistent histogram.
+    // C[l] = #{h ∈ L_h : h ≤ l}: inclusive scan of the persistent histogram. The counts
+    // are staged into the table with coalesced loads (all in flight at once), then thread t
+    // scans its contiguous run [t·per, t·per + per) in shared memory (per odd or TT = 32:
+    // the stride-per accesses hit distinct banks), one team scan of the run sums, and a
+    // second pass adds the run's offset (round 1 scanned TT entries per step: nb / TT
+    // dependent load-scan-store rounds per instance).
     const int nb = p.max_len + 1;
     const int32_t* src = p.hist + (int64_t)i * nb;
-    int carry = 0;
-    for (int x0 = 0; x0 < nb; x0 += TT) {
-      const int x = x0 + tid;
-      int v[1] = {x < nb ? __ldg(src + x) : 0}, tot[1];
-      const int own = v[0];
-      T.template excl<1>(v, tot);
-      if (x < nb) table[x] = carry + v[0] + own;
-      carry += tot[0];
+#pragma unroll 4
+    for (int x = tid; x < nb; x += TT) table[x] = __ldg(src + x);
+    T.sync();
+    const int per = (nb + TT - 1) / TT;
+    const int l0 = ::min(nb, tid * per), l1 = ::min(nb, l0 + per);
+    int run = 0;
+    for (int l = l0; l < l1; ++l) {
+      run += table[l];
+      table[l] = run;
     }
+    int v[1] = {run}, tot[1];
+    T.template excl<1>(v, tot);
+    if (v[0])
+      for (int l = l0; l < l1; ++l) table[l] += v[0];
   }
   T.sync();
 
