@@ -195,8 +195,10 @@ def relaunch_under_torchrun(args):
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")          # INIT lines show every rank joining
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if "NCCL_DEBUG" not in env:                   # INIT lines show every rank joining, on
+        env["NCCL_DEBUG"] = "INFO"                # stderr: stdout carries only the JSON line
+        env["NCCL_DEBUG_SUBSYS"] = "INIT"
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
     sys.stdout.flush()
@@ -227,8 +229,10 @@ def dist_setup(args):
         print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     if world > 1:
         import torch.distributed as dist
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if "NCCL_DEBUG" not in os.environ:
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
@@ -569,10 +573,16 @@ def main():
         }
         if cpu:
             line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
+    # release the library contexts (and their NCCL communicators) and the process group
+    # before the JSON line, so nothing follows it on stdout
+    for sc in scheds:
+        sc.close()
+    torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def measured_traffic(config, world, weak):
