@@ -643,7 +643,8 @@ admit_kernel(AdmitParams p) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int n_gt = w - bq[c];
-      const int x = bq[c] + (int)__umulhi(u[c], (uint32_t)n_gt);
+      int x;  // bq + ⌊u·n_gt / 2^32⌋ in one multiply-add of the high word
+      asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(u[c]), "r"((uint32_t)n_gt), "r"(bq[c]));
       if (LOOK == LOOK_GROUP) {
         lh[c] = (int)__ldg(p.gS + (goffS + x));  // n_gt = 0: x = W, S_g[W] = 0xFFFF sentinel
       } else if (LOOK == LOOK_SORTED) {

@@ -450,8 +450,8 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   // LOOK_SORTED coarse index: 2^cbits buckets (64: finer indexes cost more to build than
   // their shorter searches save, measured cfg 4: 256 buckets +3 %, 512 +9 %)
   c->cbits = V.TW > 1 ? PF_CIDX_BITS_MW : PF_CIDX_BITS_1;
-  if (c->layout == LAYOUT_SORTED)
-    table = (size_t)((C.window + 2) & ~1) * 2 + (size_t)((1 << c->cbits) + 2) * 2;  // u16 S + sentinel, u16 index
+  if (c->layout == LAYOUT_SORTED)  // u16 S + sentinel, then the u16 coarse index
+    table = (size_t)((C.window + 2) & ~1) * 2 + (size_t)((1 << c->cbits) + 2) * 2;
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
   c->ent_cap = (C.max_entries + 7) & ~7;
   const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
