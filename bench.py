@@ -144,6 +144,29 @@ def cpu_oracle_rate(cfg, budget_s: float, n_threads: int, seed: int, bp: int, mo
     return slots / dt, n / dt, n, slots, dt
 
 
+def cpu_fast_rate(cfg, budget_s: float, n_threads: int, seed: int, bp: int, mode: int):
+    """Context next to cpu_baseline: the optimized multithreaded CPU implementation
+    (baselines/cpu_fast.cpp: O(1) lookups, sort-form M*, binary search over the prefix)
+    on a bounded, evenly spaced sample of the workload."""
+    import baselines
+    baselines.lib()  # build outside the timed region
+
+    def run(m):
+        ids = torch.linspace(0, cfg.n_instances - 1, m).round().long().unique()
+        sub = W.make_batch(cfg, ids)
+        rows = baselines.dist_rows_of(sub)
+        t0 = time.perf_counter()
+        baselines.admit(sub, rows, mode=mode, bp=bp, seed=seed, tick=0, threads=n_threads)
+        return sub.slots(), sub.n, time.perf_counter() - t0
+
+    m = max(64, n_threads * 16)
+    slots, n, dt = run(m)
+    if dt < budget_s / 4:
+        m = int(min(cfg.n_instances, max(m, m * budget_s / max(dt, 1e-3))))
+        slots, n, dt = run(m)
+    return slots / dt, n, slots, dt
+
+
 # ------------------------------------------------------------------ reference arm (oracle)
 def run_reference(args, rank, world):
     if rank != 0:
@@ -530,7 +553,7 @@ def main():
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = slots / (float(e2e_ms[0]) * 1e-3)
 
-    cpu = None
+    cpu = cpu_fast = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nt = os.cpu_count() or 1
         rs, rd, ns, ss, dt = cpu_oracle_rate(cfg, args.cpu_budget, nt, args.seed, args.bp, args.mode)
@@ -573,6 +596,8 @@ def main():
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if cpu_fast:
+            line["cpu_fast"] = cpu_fast
     # release the library contexts (and their NCCL communicators) and the process group
     # before the JSON line, so nothing follows it on stdout
     for sc in scheds:

@@ -10,6 +10,7 @@
 #   bash tools/gpu.sh ab "LIB..." "C..." A/B of libpfsched builds (PFSCHED_LIB) per config (tools/ab.sh)
 #   bash tools/gpu.sh parity [ARGS]     tests/full_parity.py (full-size, every instance vs the oracle)
 #   bash tools/gpu.sh ubench            tools/microbench/ubench (issue rates of the ops the kernel uses)
+#   bash tools/gpu.sh sanitize          compute-sanitizer memcheck / racecheck / synccheck over GPU parity cases
 #
 # Inputs: the in-tree libpfsched.so (built by __graft_entry__.build()), alternative builds
 # for `ab` passed as paths (e.g. tools/variants/*.so from build.build(extra=[...], out=...)).
@@ -45,5 +46,15 @@ case "$mode" in
     tail -12 gpurun_out/full_parity.log ;;
   ubench)
     ./tools/microbench/ubench > gpurun_out/ubench.txt 2>&1; echo "ubench=$?" ;;
+  sanitize)
+    sel='multi_tick or empty_conditional or two_live or (variant_parity and (tw2 or tw1_unpacked or big_lmax))'
+    : > gpurun_out/sanitizer.txt
+    for tool in memcheck racecheck synccheck; do
+      echo "== compute-sanitizer --tool $tool (pytest -k \"$sel\"; one B200)" >> gpurun_out/sanitizer.txt
+      timeout 1200 compute-sanitizer --tool $tool python -m pytest tests/test_gpu_parity.py tests/test_gpu_variants.py \
+        -q -x -k "$sel" >> gpurun_out/sanitizer.txt 2>&1
+      echo "$tool=$?"
+    done
+    grep -E "SUMMARY|passed|failed" gpurun_out/sanitizer.txt ;;
   *) echo "unknown mode $mode"; exit 2 ;;
 esac

@@ -7,7 +7,7 @@ inlined helpers (pf_common.cuh hash / scans, the Team primitives, CUDA intrinsic
 inherit the phase of the nearest preceding body instruction in address order (the compiler
 lays the inlined code out at its call site).
 
-Usage: python tools/ncu_phases.py report.ncu-rep N_INSTANCES"""
+Usage: python tools/ncu_phases.py report.ncu-rep N_INSTANCES [--src pf_admit.cuh]"""
 import csv
 import os
 import re
@@ -26,8 +26,8 @@ MARKERS = [  # (regex of the first line of a section, phase)
 ]
 
 
-def sections():
-    lines = open(SRC).read().splitlines()
+def sections(src=SRC):
+    lines = open(src).read().splitlines()
     out = []
     for i, l in enumerate(lines, 1):
         for rx, ph in MARKERS:
@@ -47,7 +47,8 @@ def phase_of(line, secs, end):
 
 def main():
     rep, n = sys.argv[1], int(sys.argv[2])
-    secs, end = sections()
+    # --src FILE: the pf_admit.cuh the report was built from (e.g. an older commit's)
+    secs, end = sections(sys.argv[sys.argv.index("--src") + 1] if "--src" in sys.argv else SRC)
     first = secs[0][0]
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
