@@ -212,7 +212,7 @@ def relaunch_under_torchrun(args):
     ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
     import socket
     n_dev = torch.cuda.device_count()
-    if n_dev and args.gpus > n_dev:
+    if n_dev and args.gpus > n_dev and not SINGLE_DEVICE:
         sys.exit(f"bench.py: --gpus {args.gpus} but only {n_dev} CUDA device(s) are visible")
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
@@ -243,11 +243,23 @@ def dry_launch(args):
         print(json.dumps({"dry_launch": True, "n_gpus": world, "ranks_counted": int(n.item())}), flush=True)
 
 
+# Test hook for one-GPU boxes (tests/test_gpu_bench_multirank.py): every rank on cuda:0,
+# a gloo process group, and the shared-history exchange done by the caller (exchange
+# buffer -> torch all-reduce -> pf_commit_history) instead of the library's NCCL
+# communicator (NCCL refuses two ranks on one device). Everything else is the N-rank path.
+SINGLE_DEVICE = os.environ.get("PFBENCH_SINGLE_DEVICE") == "1"
+
+
 def dist_setup(args):
     """(rank, world, local): WORLD_SIZE from torchrun; NCCL process group with device_id."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SINGLE_DEVICE else int(os.environ.get("LOCAL_RANK", "0"))
+    if SINGLE_DEVICE and world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        return rank, world, local
     if world != args.gpus:
         print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     if world > 1:
@@ -346,13 +358,22 @@ def main():
     shards = owned_shards(cfg, rank, world) if cfg.shared else None
     bd = W.make_batch(cfg, rank=rank, nranks=world, device="cuda", shards=shards)
     torch.cuda.synchronize()
-    nccl_id = share_nccl_id(rank, world) if (cfg.shared and world > 1) else None
+    nccl_id = share_nccl_id(rank, world) if (cfg.shared and world > 1 and not SINGLE_DEVICE) else None
     # cfg2's inputs (43 MB) and per-instance histograms (34 MB) fit the 126 MB L2: rotate
     # ROT independent (context, input set) pairs so no step finds the previous one's data
     rot = 9 if args.config == 2 else 1
     sets = [bd] + [bd.clone() for _ in range(rot - 1)]
     scheds = [scheduler_for(cfg, b_, rank, world, args.mode, args.bp, args.seed, nccl_id) for b_ in sets]
     sched = scheds[0]
+    caller_exchange = bool(cfg.shared and world > 1 and nccl_id is None)  # (SINGLE_DEVICE test hook)
+
+    def exchange(sc):
+        if caller_exchange:
+            import torch.distributed as dist
+            dist.all_reduce(sc.exchange_buffer())
+            sc.commit_history()
+
+    exchange(sched)  # pf_create left the group tables for the caller's all-reduce
     pool = [W.make_completions(cfg, t, bd.row_ids) for t in range(args.tick_pool)]
     n = bd.n
     dev = "cuda"
@@ -393,6 +414,7 @@ def main():
                 side.wait_event(admit_done.pop(t - 2))
             co, cl = pool[t % len(pool)]
             sched.update_history(co, cl)
+            exchange(sched)
             e = torch.cuda.Event()
             e.record(side)
             tab_ready[t] = e
@@ -516,6 +538,7 @@ def main():
         d = dsets[t % 2]
         da, db = dcos[t % 2][j % len(hpool)]
         sched.update_history(da, db)
+        exchange(sched)
         if estimate:
             sched.estimate_peak(d["run_off"], d["input_len"], d["generated"], d["max_new"], j, peak_out=pk)
         else:
