@@ -584,6 +584,16 @@ def main():
                "sample": f"{ns} evenly spaced instances ({ss} request-slots) of {cfg.name}, one admit "
                          f"tick, oracle as it stands (Alg.1 literal, tick-stepped M*) on {nt} threads, "
                          f"{dt:.1f} s", "decisions_per_s": rd}
+        if cfg.q[1] > 0:
+            try:
+                fs, fn, fsl, fdt = cpu_fast_rate(cfg, 3.0, nt, args.seed, args.bp, args.mode)
+                cpu_fast = {"value": fs, "unit": UNIT, "cores": nt,
+                            "kind": "optimized CPU implementation (baselines/cpu_fast.cpp: O(1) lookups, "
+                                    "sort-form M*, binary search over the prefix; not the oracle)",
+                            "sample": f"{fn} evenly spaced instances ({fsl} request-slots), one admit tick, "
+                                      f"{nt} threads, {fdt:.2f} s"}
+            except Exception as ex:  # context only: never fail the bench line on it
+                cpu_fast = {"unavailable": str(ex)[:200]}
 
     if rank == 0:
         if args.config == 2:
