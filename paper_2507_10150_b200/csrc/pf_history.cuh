@@ -213,22 +213,38 @@ __global__ void update_hist_kernel(int n_rows, int row_window, int rows_per_hist
   const int lane = threadIdx.x & 31;
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (row >= n_rows) return;
+  // two memory rounds: (offsets, head), then (new values, evicted values) together; the
+  // row is validated before anything is written (round 1 had four dependent rounds)
   const int c0 = comp_off[row], c1 = comp_off[row + 1];
+  const int h = head[row];
   if (c1 == c0) return;
-  if (!row_valid(comp_len, c0, c1, max_len, lane)) {
+  const int w = row_window, c = c1 - c0;
+  if (c < 0) {
     if (lane == 0) raise_error(err, PF_BAD_COMPLETION, row);
     return;
   }
-  const int w = row_window, c = c1 - c0, m = min(c, w);
+  const int m = min(c, w);
   int32_t* R = ring + (int64_t)row * w;
   int32_t* H = hist + (int64_t)(row / rows_per_hist) * (max_len + 1);
-  const int h = head[row];
   const int first = (int)(((int64_t)h + c - m) % w);  // slot of the first surviving value
+  // the first 32 evicted values are loaded with the validation loads (same round trip)
+  int pos0 = first + lane;
+  if (pos0 >= w) pos0 -= w;
+  const int old0 = lane < m ? R[pos0] : 0;
+  bool bad = false;
+  for (int t = c0 + lane; t < c1; t += 32) {
+    const int v = comp_len[t];
+    bad |= v < 1 || v > max_len;
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0) raise_error(err, PF_BAD_COMPLETION, row);
+    return;
+  }
   for (int j = lane; j < m; j += 32) {
     int pos = first + j;
     if (pos >= w) pos -= w;
     const int v_new = comp_len[c1 - m + j];
-    const int v_old = R[pos];
+    const int v_old = j < 32 ? old0 : R[pos];
     R[pos] = v_new;
     if (v_new != v_old) {
       atomicSub(&H[v_old], 1);
@@ -245,7 +261,7 @@ __global__ void update_hist_kernel(int n_rows, int row_window, int rows_per_hist
 // loaded in one round trip, one block scan); split 0
 // stores C_g; split z fills S_g[x] for its x-range by a binary search in the shared copy
 // (one independent search per entry, no serial per-bin loops). Shared memory: 4·(Lmax+1) B.
-template <int T>
+template <int T, int MAXPER>
 __global__ void __launch_bounds__(T) group_tables_kernel(const int32_t* H, int max_len, int W,
                                                          int c_stride, int s_stride, uint16_t* gC,
                                                          uint16_t* gS) {
@@ -258,7 +274,7 @@ __global__ void __launch_bounds__(T) group_tables_kernel(const int32_t* H, int m
   uint16_t* S = gS + (int64_t)g * s_stride;
   // thread t owns the contiguous run [t·per, t·per + per): all its loads are issued at once
   // (one memory round trip), then one block scan of the run sums
-  constexpr int MAXPER = 64;  // Lmax + 1 ≤ 32768 = 512 · 64
+  // MAXPER (host-chosen) ≥ per: 16 when Lmax + 1 ≤ 16·T, else 64 (Lmax + 1 ≤ 32768 = 512·64)
   const int per = (nb + T - 1) / T;
   const int l0 = threadIdx.x * per;
   int v[MAXPER];
@@ -282,17 +298,24 @@ __global__ void __launch_bounds__(T) group_tables_kernel(const int32_t* H, int m
     }
   }
   __syncthreads();
+  // S_g: thread t fills a contiguous slice [xa, xb) of this split's range: one binary search
+  // for the slice's first entry, then a forward merge walk (S is non-decreasing in x)
   const int sper = (W + n_split - 1) / n_split;
   const int x0 = split * sper, x1 = min(W, x0 + sper);
-  for (int x = x0 + threadIdx.x; x < x1; x += T) {
-    int lo = 0, len = nb;  // first l with cum[l] > x
+  const int chunk = (x1 - x0 + T - 1) / T;
+  const int xa = x0 + threadIdx.x * chunk, xb = min(x1, xa + chunk);
+  if (xa < xb) {
+    int lo = 0, len = nb;  // first l with cum[l] > xa
     while (len > 0) {
       const int half = len >> 1;
-      const bool right = cum[lo + half] <= x;
+      const bool right = cum[lo + half] <= xa;
       lo = right ? lo + half + 1 : lo;
       len = right ? len - half - 1 : half;
     }
-    S[x] = (uint16_t)lo;
+    for (int x = xa; x < xb; ++x) {
+      while (lo < nb && cum[lo] <= x) ++lo;  // (lo = nb only if the counts sum below W)
+      S[x] = (uint16_t)lo;
+    }
   }
 }
 

@@ -187,7 +187,8 @@ pf_status build_group_tables(pf_ctx* c, cudaStream_t s) {
   const int nxt = c->tbuf ^ 1;
   const size_t G = (size_t)c->cfg.n_groups;
   const int smem = (c->cfg.max_len + 1) * 4;
-  auto fn = pf::group_tables_kernel<kTablesThreads>;
+  auto fn = (c->cfg.max_len + 1 <= 16 * kTablesThreads) ? pf::group_tables_kernel<kTablesThreads, 16>
+                                                        : pf::group_tables_kernel<kTablesThreads, 64>;
   PF_CUDA(ensure_smem(reinterpret_cast<const void*>(fn), smem));
   // one wave (one 512-thread CTA per SM): split each group's S_g fill over several CTAs
   int dev = 0, sms = 148;

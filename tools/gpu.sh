@@ -33,7 +33,8 @@ case "$mode" in
     timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
     echo "reference=$?" ;;
   launches)
-    timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
+    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
+      -k regex:"admit_kernel|group_tables|update_hist|update_sorted|init_ring|hist_rows|sort_rows" \
       python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo "launches=$?" ;;
   ncu)
     c=${1:-5}; tag=${2:-admit_cfg$c}
