@@ -47,10 +47,6 @@
 #ifndef PF_MINMAX
 #define PF_MINMAX 0
 #endif
-// Prefetch of the instance's input streams at kernel entry: 1 = L1, 2 = L2, 0 = off.
-#ifndef PF_PREFETCH
-#define PF_PREFETCH 0
-#endif
 template <bool B>
 struct BoolTag {
   static constexpr bool value = B;
@@ -145,27 +141,6 @@ __device__ __forceinline__ int bin_of(int r) {
   constexpr int SUB = flog_sub<NB>();
   const unsigned fb = __float_as_uint(__uint2float_rz((unsigned)r)) >> (23 - SUB);  // exact: r < 2^24
   return (NB - 1 + (127 << SUB)) - (int)fb;
-}
-
-// L1 prefetch of the 128-byte lines covering x[0..n), one line per thread per pass.
-__device__ __forceinline__ void prefetch_lines(const int32_t* x, int n, int tid, int tt) {
-  const uintptr_t a0 = reinterpret_cast<uintptr_t>(x) & ~(uintptr_t)127;
-  const uintptr_t a1 = reinterpret_cast<uintptr_t>(x + n);
-  for (uintptr_t a = a0 + (uintptr_t)tid * 128; a < a1; a += (uintptr_t)tt * 128)
-    if (PF_PREFETCH == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
-    else asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-}
-
-// #{x in S[0..w) : x <= v} for ascending S (upper_bound).
-__device__ __forceinline__ int upper_bound_smem(const int32_t* S, int w, int v) {
-  int lo = 0, len = w;
-  while (len > 0) {
-    int half = len >> 1;
-    bool right = S[lo + half] <= v;
-    lo = right ? lo + half + 1 : lo;
-    len = right ? len - half - 1 : half;
-  }
-  return lo;
 }
 
 // ---------------------------------------------------------------- team primitives
@@ -402,13 +377,6 @@ admit_kernel(AdmitParams p) {
   const int k = r1 - r0, q = q1 - q0, n_ent = k + q;
   const int max_new = p.max_new ? p.max_new[i] : p.max_len;
   const int cap = estimate_only ? 0 : p.capacity[i];
-  if (PF_PREFETCH && k > 0 && q >= 0 && n_ent <= p.max_entries && p.lhat_run == nullptr) {
-    // put the instance's input streams in flight now (L1 prefetch, one 128-byte line per
-    // thread): their HBM latency then overlaps the scalar chain and the shared-memory setup
-    prefetch_lines(p.input_len + r0, k, tid, TT);
-    prefetch_lines(p.generated + r0, k, tid, TT);
-    if (q > 0) prefetch_lines(p.q_input_len + q0, q, tid, TT);
-  }
   int bad = 0;
   if (k < 0 || q < 0 || n_ent > p.max_entries) bad = PF_BAD_OFFSETS;
   else if (max_new < 1 || max_new > p.max_len) bad = PF_BAD_MAX_NEW;
