@@ -33,7 +33,8 @@ import workload as W  # noqa: E402
 from harness import make_oracle, make_scheduler, np32, oracle_admit  # noqa: E402
 from workload.gen import owned_shards  # noqa: E402
 
-MODE, BP, SEED, R = 0, 500, 0x5EED, 1  # bench.py's configuration (sampling mode, R = 1, 5 %)
+MODE, BP, SEED, R = 0, 500, 0x5EED, 1  # bench.py's configuration (sampling mode, R = 1, 5 %);
+# --mode / --bp / --R override them (e.g. quantile mode, adaptive repetitions R = 0)
 
 
 def gpu_ticks(cfg, bd, ticks):
@@ -95,7 +96,7 @@ def shared_p8(cfg, ticks, ref):
         bd = W.make_batch(cfg, rank=r, nranks=P, shards=owned_shards(cfg, r, P), device="cuda")
         s = Scheduler(n_instances=bd.n, window=cfg.window, max_len=cfg.max_len, max_input_len=cfg.max_input_len,
                       max_entries=cfg.max_entries, n_groups=cfg.n_groups, group_off=bd.group_off,
-                      members_per_group=M, member_base=r * M // P, mode=MODE, reserved_bp=BP, seed=SEED,
+                      members_per_group=M, member_base=r * M // P, mode=MODE, reserved_bp=BP, seed=SEED, repetitions=R,
                       rank=r, nranks=P, init_history=bd.hist_rows)
         ranks.append((bd, s))
 
@@ -131,8 +132,14 @@ def main():
     ap.add_argument("--ticks", type=int, default=2)
     ap.add_argument("--chunk", type=int, default=1 << 14)
     ap.add_argument("--scale", type=int, default=0, help="smoke run: this many instances per config")
+    ap.add_argument("--mode", type=int, default=0, help="0 sampling (C-8), 1 quantile (u = 2^31)")
+    ap.add_argument("--bp", type=int, default=500)
+    ap.add_argument("--R", type=int, default=1, help="repetitions (0 = adaptive max(1, ceil(64/k)))")
+    ap.add_argument("--no-p8", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "full_parity.json"))
     a = ap.parse_args()
+    global MODE, BP, R
+    MODE, BP, R = a.mode, a.bp, a.R
     O.build_oracle()
     torch.cuda.set_device(0)
     results = []
@@ -151,7 +158,7 @@ def main():
                    "outputs_compared": sorted(g), "mismatches": bad, "seconds": round(time.time() - t0, 1)}
             print(json.dumps(rec), flush=True)
             results.append(rec)
-        if cfg.shared:
+        if cfg.shared and not a.no_p8:
             del bd
             torch.cuda.empty_cache()
             bad8 = shared_p8(cfg, a.ticks, ref)
