@@ -2,7 +2,9 @@
 DESIGN.md §7): rank 0's shard (2^20 / P instances, owned history shards s ≡ 0 mod P) runs
 bench.py's pipelined step — update_history + group tables on a side stream overlapping the
 admit — with the exchange replaced by the caller-side commit of the local partial sums (the
-NCCL all-reduce of the 1.3 MB buffer is the one part not timed here). Prints per P: admit ms,
+NCCL all-reduce of the 1.3 MB buffer is emulated by a device copy of the exact all-reduced
+histogram, kept by a one-member-per-group reference context fed every shard's completions).
+Prints per P: admit ms,
 step ms, and the strong-scaling efficiency t(1) / (P · t(P)) the compute alone allows.
 
   python tools/shard_probe.py [--steps 50]"""
@@ -20,6 +22,9 @@ from workload.gen import owned_shards  # noqa: E402
 from paper_2507_10150_b200 import Scheduler  # noqa: E402
 
 
+PRIO = int(os.environ.get("PROBE_SIDE_PRIORITY", "-1"))  # bench.py's choice; 0 = default priority
+
+
 def run(P, steps):
     cfg = W.CONFIGS[5]
     M = cfg.members_per_group
@@ -28,12 +33,22 @@ def run(P, steps):
                   max_entries=cfg.max_entries, n_groups=cfg.n_groups, group_off=bd.group_off,
                   members_per_group=M, member_base=0, mode=0, reserved_bp=500, seed=0x5EED, rank=0,
                   nranks=P, init_history=bd.hist_rows)
+    # the all-reduced group histograms H_g: a reference context holding every shard row
+    full = W.make_batch(W.scaled(cfg, cfg.n_groups), device="cuda")
+    ref = Scheduler(n_instances=full.n, window=cfg.window, max_len=cfg.max_len, max_input_len=cfg.max_input_len,
+                    max_entries=cfg.max_entries, n_groups=cfg.n_groups, group_off=full.group_off,
+                    members_per_group=1, member_base=0, mode=0, reserved_bp=500, seed=0x5EED,
+                    init_history=full.hist_rows)
+    xb, xr = s.exchange_buffer(), ref.exchange_buffer()
+    xb.copy_(xr)
     s.commit_history()
     pool = [W.make_completions(cfg, t, bd.row_ids) for t in range(16)]
+    rpool = [W.make_completions(cfg, t, full.row_ids) for t in range(16)]
     n = bd.n
     adm = torch.empty(n, dtype=torch.int32, device="cuda")
     pk = torch.empty_like(adm)
-    main, side = torch.cuda.current_stream(), torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream(priority=PRIO)  # -1: high priority (its CTAs dispatch ahead of admit's)
     ready, done = {}, {}
 
     def tables(t):
@@ -43,6 +58,8 @@ def run(P, steps):
             co, cl = pool[t % 16]
             s.update_history(co, cl)
             if P > 1:
+                ref.update_history(*rpool[t % 16])
+                xb.copy_(xr)  # stands in for ncclAllReduce(sum) of the partial histograms
                 s.commit_history()
             e = torch.cuda.Event()
             e.record(side)
@@ -67,17 +84,21 @@ def run(P, steps):
     torch.cuda.synchronize()
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import time
     e0.record(main)
+    h0 = time.perf_counter()
     for j in range(steps):
         admit(5 + j, kev[j])
         tables(6 + j)
+    host_ms = (time.perf_counter() - h0) * 1e3 / steps
     main.wait_event(ready[5 + steps])
     e1.record(main)
     torch.cuda.synchronize()
     step = e0.elapsed_time(e1) / steps
     adm_ms = sum(a.elapsed_time(b) for a, b in kev) / steps
     s.close()
-    return n, bd.slots(), adm_ms, step
+    ref.close()
+    return n, bd.slots(), adm_ms, step, host_ms
 
 
 def main():
@@ -87,10 +108,11 @@ def main():
     torch.cuda.set_device(0)
     base = None
     for P in (1, 2, 4, 8):
-        n, slots, adm_ms, step = run(P, a.steps)
+        n, slots, adm_ms, step, host_ms = run(P, a.steps)
         base = base or step
         print(json.dumps({"P": P, "instances_per_rank": n, "slots_per_rank": slots, "admit_ms": round(adm_ms, 4),
-                          "step_ms": round(step, 4), "compute_strong_scaling_eff": round(base / (P * step), 3)}),
+                          "step_ms": round(step, 4), "host_enqueue_ms_per_step": round(host_ms, 4),
+                          "compute_strong_scaling_eff": round(base / (P * step), 3)}),
               flush=True)
 
 
