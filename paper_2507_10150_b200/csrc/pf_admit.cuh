@@ -143,6 +143,21 @@ __device__ __forceinline__ int bin_of(int r) {
   return (NB - 1 + (127 << SUB)) - (int)fb;
 }
 
+// Request-input loads: read once, so PF_STREAM_NA = 1 keeps them out of L1
+// (L1::no_allocate) to leave L1 to the group tables.
+#ifndef PF_STREAM_NA
+#define PF_STREAM_NA 1
+#endif
+__device__ __forceinline__ int ld_stream(const int32_t* a) {
+  if constexpr (PF_STREAM_NA) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(a));
+    return v;
+  } else {
+    return __ldg(a);
+  }
+}
+
 // ---------------------------------------------------------------- team primitives
 template <int TW>
 struct Team {
@@ -575,12 +590,12 @@ admit_kernel(AdmitParams p) {
     for (int c = 0; c < NC; ++c) {
       const int e = e0 + c * TT;
       if (FAST) {  // the whole chunk is running requests: no guards, no selects
-        lp[c] = __ldg(lpR + e);
-        lt[c] = __ldg(ltR + e);
+        lp[c] = ld_stream(lpR + e);
+        lt[c] = ld_stream(ltR + e);
       } else {
         const bool run = e < k;
-        lp[c] = (e < n_ent) ? __ldg((run ? lpR : lpQ) + e) : 0;
-        lt[c] = run ? __ldg(ltR + e) : 0;
+        lp[c] = (e < n_ent) ? ld_stream((run ? lpR : lpQ) + e) : 0;
+        lt[c] = run ? ld_stream(ltR + e) : 0;
       }
     }
 #pragma unroll
