@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpfsched.so")
 SOURCES = ["pfsched.cu"]
-HEADERS = ["pf_common.cuh", "pf_admit.cuh", "pf_history.cuh", "pf_baseline.cuh", "pf_sim.cuh",
+HEADERS = ["pf_common.cuh", "pf_admit.cuh", "pf_admit_group.cuh", "pf_history.cuh", "pf_baseline.cuh", "pf_sim.cuh",
            "pf_analysis.cuh", "pf_forward.cuh"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

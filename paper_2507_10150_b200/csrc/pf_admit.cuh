@@ -99,6 +99,9 @@ struct AdmitParams {
   const uint16_t* gC;        // LOOK_GROUP  [G × c_stride]: C_g[l] = #{h ≤ l} (u16, W < 2^16)
   const uint16_t* gS;        // LOOK_GROUP  [G × s_stride]: sorted group window (u16)
   int c_stride, s_stride;    // row strides (multiples of 8 elements)
+  int n_groups;              // G (shared mode)
+  unsigned long long* gcost; // admit_group_kernel: [3][2·G] per-group cycles, counts (rotating)
+  uint32_t cost_epoch;       // launch counter selecting the rotating cost buffers
   int cbits;                 // LOOK_SORTED: log2 of the coarse-index bucket count
   int csh;                   // LOOK_SORTED: bucket width 2^csh, smallest with (Lmax+1) >> csh ≤ 2^cbits
   const int32_t* dist_of;    // LOOK_GROUP  [n]
@@ -326,7 +329,6 @@ struct Eval {
 //   xs[140] i32      scratch: reductions [0,32), pick [32,34), list size [36], candidates [40,137)
 //   table            S[w+1] u16 + coarse index cidx[2^cbits + 2] u16 (LOOK_SORTED) | C[Lmax+1] i32 (LOOK_HIST)
 // (the per-bin r ranges `edges` are read through L1 from global memory: 512 B per launch)
-template <int TW, int LOOK, int PK>
 // Resident 4-team CTAs per SM for one-warp teams (register cap 65536 / (128 · PF_MIN_CTAS)):
 // 9 → 56 registers, measured best on cfg5 (8: −4 %, 10: spills, +60 %).
 #ifndef PF_MIN_CTAS
@@ -346,8 +348,10 @@ template <int TW, int LOOK, int PK>
 #if PF_LOCKSTEP_MAX > 16
 #error "PF_LOCKSTEP_MAX > 16 overflows the candidate table"
 #endif
-__global__ void __launch_bounds__((TW == 1 ? PF_TEAMS1 : 1) * TW * 32, (TW == 1 ? PF_MIN_CTAS : (PF_MW_WARPS / TW > 1 ? PF_MW_WARPS / TW : 1)))
-admit_kernel(AdmitParams p) {
+// One instance i on team T (the whole of a4-a8 for that instance).
+template <int TW, int LOOK, int PK>
+__device__ __forceinline__ void admit_one(const AdmitParams& p, Team<TW>& T, unsigned char* base,
+                                          const int i) {
   constexpr int TT = TW * 32;
   constexpr int BPT = PF_BPT;  // bins per thread
   constexpr int NB = 32 * BPT * TW;
@@ -357,14 +361,6 @@ admit_kernel(AdmitParams p) {
   constexpr int NSH = PK ? PK : 9;
   constexpr uint32_t NMASK = (1u << NSH) - 1u;
   constexpr int NBW = PACK ? NB : 2 * NB;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-
-  Team<TW> T;
-  T.id = threadIdx.x / TT;
-  T.tid = threadIdx.x % TT;
-  T.lane = threadIdx.x & 31;
-  T.wid = T.tid >> 5;
-  unsigned char* base = smem_raw + (size_t)T.id * p.team_smem;
   uint32_t* rb = reinterpret_cast<uint32_t*>(base);
   int* av = reinterpret_cast<int*>(rb + p.ent_cap);  // unused when PACK
   uint16_t* nx = reinterpret_cast<uint16_t*>(av + (PACK ? 0 : p.ent_cap));
@@ -380,8 +376,6 @@ admit_kernel(AdmitParams p) {
   int32_t* table = T.xs + 140;
   uint16_t* tS = reinterpret_cast<uint16_t*>(table);  // LOOK_SORTED: the window, u16 (Lmax < 2^16)
 
-  const int i = blockIdx.x * (TW == 1 ? p.teams : 1) + T.id;
-  if (i >= p.n) return;
   const int tid = T.tid;
   const bool estimate_only = (p.q_off == nullptr);
 
@@ -412,7 +406,13 @@ admit_kernel(AdmitParams p) {
     return;
   }
   // C = the largest integer M* that fits: 10^4·M* ≤ (10^4 − bp)·cap (C-12, C-13).
-  const int Cmax = estimate_only ? 0 : (int)(((int64_t)(10000 - p.bp) * cap) / 10000);
+  // In 32-bit arithmetic: with cap = 10^4·Q + R, ⌊m·cap/10^4⌋ = m·Q + ⌊m·R/10^4⌋ (m ≤ 10^4,
+  // so m·Q ≤ cap·m/10^4 < 2^31 and m·R < 10^8).
+  int Cmax = 0;
+  if (!estimate_only) {
+    const uint32_t m = 10000u - (uint32_t)p.bp, cu = (uint32_t)cap;
+    Cmax = (int)(m * (cu / 10000u) + (m * (cu % 10000u)) / 10000u);
+  }
 
   // ---- a3: the distribution P(l) of Eq.(eq:5) as a lookup structure
   const int w = p.w;
@@ -1041,6 +1041,23 @@ admit_kernel(AdmitParams p) {
     p.peak_out[i] = peak;
     if (p.peak_running_out) p.peak_running_out[i] = M0;
   }
+}
+
+// One team per instance, several teams per CTA (LOOK_SORTED / LOOK_HIST / LOOK_GROUP).
+template <int TW, int LOOK, int PK>
+__global__ void __launch_bounds__((TW == 1 ? PF_TEAMS1 : 1) * TW * 32, (TW == 1 ? PF_MIN_CTAS : (PF_MW_WARPS / TW > 1 ? PF_MW_WARPS / TW : 1)))
+admit_kernel(AdmitParams p) {
+  constexpr int TT = TW * 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Team<TW> T;
+  T.id = threadIdx.x / TT;
+  T.tid = threadIdx.x % TT;
+  T.lane = threadIdx.x & 31;
+  T.wid = T.tid >> 5;
+  unsigned char* base = smem_raw + (size_t)T.id * p.team_smem;
+  const int i = blockIdx.x * (TW == 1 ? p.teams : 1) + T.id;
+  if (i >= p.n) return;
+  admit_one<TW, LOOK, PK>(p, T, base, i);
 }
 
 }  // namespace pf

@@ -15,6 +15,7 @@
 
 #include "../../include/pfsched.h"
 #include "pf_admit.cuh"  // defines PF_BPT, PF_MINMAX, PF_LOCKSTEP_MAX
+#include "pf_admit_group.cuh"
 #include "pf_baseline.cuh"
 #include "pf_history.cuh"
 #include "pf_sim.cuh"
@@ -124,6 +125,11 @@ struct pf_ctx {
   int teams;           // instance teams per CTA of the admit kernel
   int carveout;        // preferred shared-memory carve-out (%) of the admit kernel, −1 = none
   bool committed = false;  // group tables built at least once (shared mode)
+  int gp_warps = 0;        // admit_group_kernel: one-warp teams per CTA (0 = not used)
+  size_t gp_smem = 0;      // its shared memory per CTA (tables + teams)
+  int sms = 148;           // SMs of the context's device (one admit_group_kernel CTA each)
+  unsigned long long* gcost = nullptr;  // [3][2·G] admit_group_kernel cost buffers
+  uint32_t cost_epoch = 0;              // admit_group_kernel launches so far
   void* comm = nullptr;    // ncclComm_t owned by the context (shared mode, nccl_unique_id set)
 };
 
@@ -136,7 +142,7 @@ void free_ctx(pf_ctx* c) {
   for (void* p : {(void*)c->ring, (void*)c->head, (void*)c->sorted, (void*)c->hist,
                   (void*)c->xbuf, (void*)c->gC, (void*)c->gS, (void*)c->dist_of,
                   (void*)c->group_off, (void*)c->err, (void*)c->scratch,
-                  (void*)c->edges})
+                  (void*)c->edges, (void*)c->gcost})
     if (p) cudaFree(p);
   if (c->comm) nccl_destroy(c->comm);
   delete c;
@@ -470,6 +476,29 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     fail(PF_ERANGE, "admit kernel needs %zu B of shared memory per instance team (> 227 KB)", c->admit_smem);
     return cleanup_fail(PF_ERANGE);
   }
+  // Shared mode, one-warp teams, packed bins: the persistent admit_group_kernel with the
+  // group tables in shared memory (pf_admit.cuh), when the tables leave room for ≥ 8 teams.
+  // PFSCHED_GROUP_KERNEL=0 selects the cached-table admit_kernel instead (A/B measurements).
+  if (c->layout == LAYOUT_GROUP && V.TW == 1 && c->pack != 0) {
+    const char* ev = getenv("PFSCHED_GROUP_KERNEL");
+    const size_t tables = (size_t)(c->c_stride + c->s_stride) * 2 + 32;
+    const size_t avail = 232448;  // 227 KB opt-in maximum per block
+    const int nw = avail > tables ? (int)std::min<size_t>(32, (avail - tables) / team) : 0;
+    if (nw >= 8 && !(ev && ev[0] == '0')) {
+      c->gp_warps = nw;
+      c->gp_smem = tables + (size_t)nw * team;
+      const void* gfn = c->pack == 1 ? reinterpret_cast<const void*>(pf::admit_group_kernel<9>)
+                                     : reinterpret_cast<const void*>(pf::admit_group_kernel<10>);
+      PF_CUDA_C(ensure_smem(gfn, (int)c->gp_smem));
+      int dev = 0;
+      PF_CUDA_C(cudaGetDevice(&dev));
+      PF_CUDA_C(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
+      if (C.n_groups <= 256) {
+        PF_CUDA_C(cudaMalloc(&c->gcost, (size_t)6 * C.n_groups * 8));
+        PF_CUDA_C(cudaMemsetAsync(c->gcost, 0, (size_t)6 * C.n_groups * 8, s));
+      }
+    }
+  }
   const void* afn = reinterpret_cast<const void*>(V.fn[look][c->pack]);
   PF_CUDA_C(ensure_smem(afn, (int)c->admit_smem));
 #ifndef PF_CARVEOUT
@@ -588,6 +617,7 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.csh = 0;
   while (((C.max_len + 1) >> p.csh) > (1 << c->cbits)) ++p.csh;
   p.s_stride = c->s_stride;
+  p.n_groups = C.n_groups;
   p.dist_of = c->dist_of;
   p.group_off = c->group_off;
   p.run_off = run_off;
@@ -605,6 +635,20 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.lhat_run = lhat_run;
   p.lhat_q = lhat_q;
   p.err = c->err;
+  if (c->gp_warps && !lhat_run) {
+    const void* gfn = c->pack == 1 ? reinterpret_cast<const void*>(pf::admit_group_kernel<9>)
+                                   : reinterpret_cast<const void*>(pf::admit_group_kernel<10>);
+    PF_CUDA(ensure_smem(gfn, (int)c->gp_smem));
+    const int grid = std::max(1, std::min(c->sms, C.n_instances));
+    p.gcost = c->gcost;
+    p.cost_epoch = c->cost_epoch++;
+    if (c->pack == 1)
+      pf::admit_group_kernel<9><<<grid, c->gp_warps * 32, c->gp_smem, s>>>(p);
+    else
+      pf::admit_group_kernel<10><<<grid, c->gp_warps * 32, c->gp_smem, s>>>(p);
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+  }
   const Variant& V = kVariants[c->variant];
   const int teams = c->teams;
   p.teams = teams;

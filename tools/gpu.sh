@@ -11,6 +11,10 @@
 #   bash tools/gpu.sh parity [ARGS]     tests/full_parity.py (full-size, every instance vs the oracle)
 #   bash tools/gpu.sh ubench            tools/microbench/ubench (issue rates of the ops the kernel uses)
 #   bash tools/gpu.sh sanitize          compute-sanitizer memcheck / racecheck / synccheck over GPU parity cases
+#   bash tools/gpu.sh profile TAG [C]   ncu --set full of the 4th admit launch of config C (default 5) + raw / SASS csv
+#                                       (read here with tools/ncu_keys.py, tools/sass_hist.py, tools/sass_blocks.py)
+#   bash tools/gpu.sh groupab           bench cfg 5 with admit_group_kernel (default) and with admit_kernel
+#                                       (PFSCHED_GROUP_KERNEL=0) on one box
 #
 # Inputs: the in-tree libpfsched.so (built by __graft_entry__.build()), alternative builds
 # for `ab` passed as paths (e.g. tools/variants/*.so from build.build(extra=[...], out=...)).
@@ -57,5 +61,16 @@ case "$mode" in
       echo "$tool=$?"
     done
     grep -E "SUMMARY|passed|failed" gpurun_out/sanitizer.txt ;;
+  profile)
+    tag=${1:-prof}; c=${2:-5}
+    timeout 600 ncu --set full --import-source on --clock-control none -k regex:admit --launch-skip 3 -c 1 \
+      -o "gpurun_out/$tag" python tools/prof_admit.py --config "$c" --ticks 4 > "gpurun_out/$tag.log" 2>&1; echo ncu=$?
+    ncu -i "gpurun_out/$tag.ncu-rep" --page raw --csv > "gpurun_out/${tag}_raw.csv" 2>&1
+    ncu -i "gpurun_out/$tag.ncu-rep" --page source --csv --print-source sass > "gpurun_out/${tag}_sass.csv" 2>&1 ;;
+  groupab)
+    for v in 1 0; do
+      PFSCHED_GROUP_KERNEL=$v timeout 300 python bench.py --no-cpu-baseline --e2e-steps 1 --steps 100 --warmup 5 2>/dev/null \
+        | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('group_kernel=$v', 'admit_ms', round(d['config']['admit_kernel_ms'], 4), 'step_ms', round(d['ms_per_step'], 4), d['config']['output_check'])"
+    done ;;
   *) echo "unknown mode $mode"; exit 2 ;;
 esac
