@@ -53,6 +53,12 @@ __device__ __forceinline__ void red_add_sh_if(uint32_t a, uint32_t v, bool p) {
                :: "r"(a), "r"(v), "r"((int)p) : "memory");
 }
 
+__device__ __forceinline__ uint32_t atom_add_sh(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t x;
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(a), "r"(b), "r"(c));
@@ -212,9 +218,20 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       for (; e0 + 4 * 32 <= k; e0 += 4 * 32)
         chunk(e0, k, lpR + e0, ltR + e0, poR ? poR + e0 : nullptr, binR, BoolTag<true>(), fast_tag,
               IntTag<4>(), BoolTag<true>());
+      // ragged tail (< 128 requests): 2-, 1- and one predicated 1-request-per-lane chunks
+      if (e0 + 2 * 32 <= k) {
+        chunk(e0, k, lpR + e0, ltR + e0, poR ? poR + e0 : nullptr, binR, BoolTag<true>(), fast_tag,
+              IntTag<2>(), BoolTag<true>());
+        e0 += 2 * 32;
+      }
+      if (e0 + 32 <= k) {
+        chunk(e0, k, lpR + e0, ltR + e0, poR ? poR + e0 : nullptr, binR, BoolTag<true>(), fast_tag,
+              IntTag<1>(), BoolTag<true>());
+        e0 += 32;
+      }
       if (e0 < k)
         chunk(e0, k, lpR + e0, ltR + e0, poR ? poR + e0 : nullptr, binR, BoolTag<false>(), fast_tag,
-              IntTag<4>(), BoolTag<true>());
+              IntTag<1>(), BoolTag<true>());
     };
     if (draw_fast) run_loop(BoolTag<true>());
     else run_loop(BoolTag<false>());
@@ -228,9 +245,14 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       for (; j0 + 2 * 32 <= q; j0 += 2 * 32)
         chunk(j0, q, lpQ + j0, nullptr, poQ ? poQ + j0 : nullptr, binQ, BoolTag<true>(), fast_tag,
               IntTag<2>(), BoolTag<false>());
+      if (j0 + 32 <= q) {
+        chunk(j0, q, lpQ + j0, nullptr, poQ ? poQ + j0 : nullptr, binQ, BoolTag<true>(), fast_tag,
+              IntTag<1>(), BoolTag<false>());
+        j0 += 32;
+      }
       if (j0 < q)
         chunk(j0, q, lpQ + j0, nullptr, poQ ? poQ + j0 : nullptr, binQ, BoolTag<false>(), fast_tag,
-              IntTag<2>(), BoolTag<false>());
+              IntTag<1>(), BoolTag<false>());
     };
     if (draw_fast) q_loop(BoolTag<true>());
     else q_loop(BoolTag<false>());
@@ -517,18 +539,20 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
 // first launch (no measurements) splits by instance count. The partition only decides
 // which CTA computes an instance; every output is the same bit for bit.
 // (buffers: launch t reads cost[(t+2) % 3], adds to cost[t % 3], zeroes cost[(t+1) % 3])
-__device__ __forceinline__ int cost_cut(const AdmitParams& p, const float* wg, float total, int b) {
-  // instance index at cumulative weight b·total/grid (b = grid → n)
+__device__ __forceinline__ int cost_cut(const AdmitParams& p, const float* wg, const float* cum, int b) {
+  // instance index at cumulative weight b·total/grid (b = grid → n); cum[g] = weight of
+  // groups < g, cum[G] = total
+  const int G = p.n_groups;
   if (b >= (int)gridDim.x) return p.n;
-  const float t = total * (float)b / (float)gridDim.x;
-  float acc = 0.f;
-  for (int g = 0; g < p.n_groups; ++g) {
-    const int o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
-    const float c = wg[g] * (float)(o1 - o0);
-    if (acc + c > t) return ::min(o1, o0 + (int)((t - acc) / wg[g]));
-    acc += c;
+  const float t = cum[G] * (float)b / (float)gridDim.x;
+  int g = 0, len = G;  // last g with cum[g] ≤ t
+  while (len > 1) {
+    const int half = len >> 1;
+    if (cum[g + half] <= t) g += half;
+    len -= half;
   }
-  return p.n;
+  const int o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
+  return ::min(o1, o0 + (int)((t - cum[g]) / wg[g]));
 }
 
 // Persistent CTA per SM (header comment). Shared memory: C_g u16 [c_stride] | S_g u16
@@ -539,10 +563,10 @@ __global__ void __launch_bounds__(1024, 1) admit_group_kernel(AdmitParams p) {
   uint16_t* sC = reinterpret_cast<uint16_t*>(smem_raw);
   uint16_t* sS = sC + p.c_stride;
   // control: [0] next instance, [1] lo, [2] hi, [3] group of the open cost segment,
-  // [4..5] u64 cycles and [6] instances of that segment
+  // [4] SM cycles (u32: < 2^32 per CTA segment) and [5] instances of that segment
   int* ctl = reinterpret_cast<int*>(sS + p.s_stride);
-  unsigned long long* seg_cyc = reinterpret_cast<unsigned long long*>(ctl + 4);
-  unsigned int* seg_cnt = reinterpret_cast<unsigned int*>(ctl + 6);
+  unsigned int* seg_cyc = reinterpret_cast<unsigned int*>(ctl + 4);
+  unsigned int* seg_cnt = reinterpret_cast<unsigned int*>(ctl + 5);
   const int lane = threadIdx.x & 31;
   unsigned char* base = reinterpret_cast<unsigned char*>(ctl + 8) + (size_t)(threadIdx.x >> 5) * p.team_smem;
   const int G = p.n_groups;
@@ -551,43 +575,68 @@ __global__ void __launch_bounds__(1024, 1) admit_group_kernel(AdmitParams p) {
     unsigned long long* z = p.gcost + (size_t)((p.cost_epoch + 1) % 3) * 2 * G;
     for (int x = threadIdx.x; x < 2 * G; x += blockDim.x) z[x] = 0ull;
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: this CTA's range
     int lo = (int)(((int64_t)blockIdx.x * p.n) / gridDim.x);
     int hi = (int)(((int64_t)(blockIdx.x + 1) * p.n) / gridDim.x);
     if (p.gcost && G <= 256) {
       const unsigned long long* rd = p.gcost + (size_t)((p.cost_epoch + 2) % 3) * 2 * G;
       float* wg = reinterpret_cast<float*>(base);  // team 0's area, free until the barrier below
-      float sw = 0.f, total = 0.f;
-      int nw = 0;
-      for (int g = 0; g < G; ++g) {
+      float* cum = wg + G;                         // [G + 1]
+      float sw = 0.f, nw = 0.f;
+      for (int g = lane; g < G; g += 32) {
         const unsigned long long cnt = rd[G + g];
-        wg[g] = cnt ? (float)rd[g] / (float)cnt : 0.f;
-        if (cnt) { sw += wg[g]; ++nw; }
-      }
-      if (nw > 0) {
-        const float mean = sw / (float)nw;
-        for (int g = 0; g < G; ++g) {
-          if (wg[g] <= 0.f) wg[g] = mean;
-          total += wg[g] * (float)(__ldg(p.group_off + g + 1) - __ldg(p.group_off + g));
+        const float w = cnt ? (float)rd[g] / (float)cnt : 0.f;
+        wg[g] = w;
+        if (cnt) {
+          sw += w;
+          nw += 1.f;
         }
-        lo = cost_cut(p, wg, total, blockIdx.x);
-        hi = cost_cut(p, wg, total, blockIdx.x + 1);
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        sw += __shfl_xor_sync(0xffffffffu, sw, d);
+        nw += __shfl_xor_sync(0xffffffffu, nw, d);
+      }
+      if (nw > 0.f) {
+        const float mean = sw / nw;
+        float carry = 0.f;
+        for (int g0 = 0; g0 < G; g0 += 32) {
+          const int g = g0 + lane;
+          float c = 0.f;
+          if (g < G) {
+            if (wg[g] <= 0.f) wg[g] = mean;
+            c = wg[g] * (float)(__ldg(p.group_off + g + 1) - __ldg(p.group_off + g));
+          }
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const float t = __shfl_up_sync(0xffffffffu, c, d);
+            if (lane >= d) c += t;
+          }
+          if (g < G) cum[g + 1] = carry + c;
+          carry += __shfl_sync(0xffffffffu, c, 31);
+        }
+        if (lane == 0) cum[0] = 0.f;
+        __syncwarp();
+        lo = cost_cut(p, wg, cum, blockIdx.x);
+        hi = cost_cut(p, wg, cum, blockIdx.x + 1);
       }
     }
-    ctl[1] = lo;
-    ctl[2] = ::max(lo, hi);
-    ctl[3] = -1;
-    *seg_cyc = 0ull;
-    *seg_cnt = 0u;
+    if (lane == 0) {
+      ctl[1] = lo;
+      ctl[2] = ::max(lo, hi);
+      ctl[3] = -1;
+      *seg_cyc = 0u;
+      *seg_cnt = 0u;
+    }
   }
   __syncthreads();
   // thread 0, all warps past the segment: add the open segment's cost to its group
   auto flush_cost = [&]() {
     if (cost_wr && ctl[3] >= 0 && *seg_cnt) {
-      atomicAdd(cost_wr + ctl[3], *seg_cyc);
+      atomicAdd(cost_wr + ctl[3], (unsigned long long)*seg_cyc);
       atomicAdd(cost_wr + G + ctl[3], (unsigned long long)*seg_cnt);
     }
-    *seg_cyc = 0ull;
+    *seg_cyc = 0u;
     *seg_cnt = 0u;
   };
   const int lo = ctl[1], hi = ctl[2];
@@ -625,18 +674,19 @@ __global__ void __launch_bounds__(1024, 1) admit_group_kernel(AdmitParams p) {
     }
     __syncthreads();
     const int64_t gid_base = (int64_t)g * p.members_per_group + p.member_base - __ldg(p.group_off + g);
+    const uint32_t a_ctl = sh_addr(ctl);
 #pragma unroll 1
     for (;;) {
       __syncwarp();  // the previous instance's shared-memory reads are done
       int i = 0;
-      if (lane == 0) i = atomicAdd(ctl, 1);
+      if (lane == 0) i = (int)atom_add_sh(a_ctl, 1u);
       i = __shfl_sync(0xffffffffu, i, 0);
       if (i >= s_hi) break;
-      const long long t0 = clock64();
+      const uint32_t t0 = (uint32_t)clock();
       group_one<PK>(p, lane, base, i, sC, sS, gid_base);
       if (cost_wr && lane == 0) {
-        atomicAdd(seg_cyc, (unsigned long long)(clock64() - t0));
-        atomicAdd(seg_cnt, 1u);
+        atom_add_sh(a_ctl + 16u, (uint32_t)clock() - t0);
+        atom_add_sh(a_ctl + 20u, 1u);
       }
     }
     s_lo = s_hi;
