@@ -69,7 +69,7 @@ __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
 //   rb[ent_cap] u32 records r | a << 13 (slot e: running e < k, queued k + j)
 //   nx[ent_cap] u16 per-bin request lists, hd[128] u32 list heads
 //   binR[128], binQ[128] u32 packed (A << PK | N) per r-bin, xs[140] i32 scratch
-template <int PK>
+template <int PK, bool EST>
 __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, unsigned char* base,
                                           const int i, const uint16_t* sC, const uint16_t* sS,
                                           const int64_t gid_base) {
@@ -85,7 +85,7 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   int* cand = xs + 40;  // [0]: count, then 6 ints per candidate (≤ 16)
   auto ent_r = [&](int e) -> int { return (int)(rb[e] & 0x1FFFu); };
   auto ent_a = [&](int e) -> int { return (int)(rb[e] >> 13); };
-  const bool estimate_only = (p.q_off == nullptr);
+  constexpr bool estimate_only = EST;  // pf_estimate_peak (no queue, no capacity)
 
   // ---- instance scalars and CSR validation
   const int r0 = __ldg(p.run_off + i), r1 = __ldg(p.run_off + i + 1);
@@ -153,7 +153,7 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   const uint32_t bq0 = sC[0];
   const uint32_t a_rb = sh_addr(rb), a_nx = sh_addr(nx), a_hd = sh_addr(hd);
   auto chunk = [&](const int e0, const int n, const int32_t* lpp, const int32_t* ltp,
-                   int32_t* po, uint32_t* bins, auto full_tag, auto fast_tag, auto nc_tag,
+                   int32_t* po_base, uint32_t* bins, auto full_tag, auto fast_tag, auto nc_tag,
                    auto run_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
     constexpr bool FAST = decltype(fast_tag)::value;  // sampling mode, R = 1
@@ -202,7 +202,8 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
         red_add_sh_if(sh_addr(bins) + b4, an, ok[c]);
       }
     }
-    if (po) {  // prediction outputs (one uniform branch per chunk)
+    if (po_base) {  // prediction outputs (one uniform branch per chunk)
+      int32_t* po = po_base + e0;
 #pragma unroll
       for (int c = 0; c < NC; ++c)
         if (FULL || ok[c]) po[c * 32] = lh[c];
@@ -211,26 +212,26 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   {
     const int32_t* lpR = p.input_len + r0 + lane;
     const int32_t* ltR = p.generated + r0 + lane;
-    int32_t* poR = p.pred_run_out ? p.pred_run_out + r0 + lane : nullptr;
+    int32_t* poR = p.pred_run_out ? p.pred_run_out + (r0 + lane) : nullptr;
     auto run_loop = [&](auto fast_tag) {
       int e0 = 0;
 #pragma unroll 1
       for (; e0 + 4 * 32 <= k; e0 += 4 * 32)
-        chunk(e0, k, lpR + e0, ltR + e0, poR ? poR + e0 : nullptr, binR, BoolTag<true>(), fast_tag,
+        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<true>(), fast_tag,
               IntTag<4>(), BoolTag<true>());
       // ragged tail (< 128 requests): 2-, 1- and one predicated 1-request-per-lane chunks
       if (e0 + 2 * 32 <= k) {
-        chunk(e0, k, lpR + e0, ltR + e0, poR ? poR + e0 : nullptr, binR, BoolTag<true>(), fast_tag,
+        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<true>(), fast_tag,
               IntTag<2>(), BoolTag<true>());
         e0 += 2 * 32;
       }
       if (e0 + 32 <= k) {
-        chunk(e0, k, lpR + e0, ltR + e0, poR ? poR + e0 : nullptr, binR, BoolTag<true>(), fast_tag,
+        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<true>(), fast_tag,
               IntTag<1>(), BoolTag<true>());
         e0 += 32;
       }
       if (e0 < k)
-        chunk(e0, k, lpR + e0, ltR + e0, poR ? poR + e0 : nullptr, binR, BoolTag<false>(), fast_tag,
+        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<false>(), fast_tag,
               IntTag<1>(), BoolTag<true>());
     };
     if (draw_fast) run_loop(BoolTag<true>());
@@ -238,20 +239,20 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   }
   if (!estimate_only) {
     const int32_t* lpQ = p.q_input_len + q0 + lane;
-    int32_t* poQ = p.pred_q_out ? p.pred_q_out + q0 + lane : nullptr;
+    int32_t* poQ = p.pred_q_out ? p.pred_q_out + (q0 + lane) : nullptr;
     auto q_loop = [&](auto fast_tag) {
       int j0 = 0;
 #pragma unroll 1
       for (; j0 + 2 * 32 <= q; j0 += 2 * 32)
-        chunk(j0, q, lpQ + j0, nullptr, poQ ? poQ + j0 : nullptr, binQ, BoolTag<true>(), fast_tag,
+        chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<true>(), fast_tag,
               IntTag<2>(), BoolTag<false>());
       if (j0 + 32 <= q) {
-        chunk(j0, q, lpQ + j0, nullptr, poQ ? poQ + j0 : nullptr, binQ, BoolTag<true>(), fast_tag,
+        chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<true>(), fast_tag,
               IntTag<1>(), BoolTag<false>());
         j0 += 32;
       }
       if (j0 < q)
-        chunk(j0, q, lpQ + j0, nullptr, poQ ? poQ + j0 : nullptr, binQ, BoolTag<false>(), fast_tag,
+        chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<false>(), fast_tag,
               IntTag<1>(), BoolTag<false>());
     };
     if (draw_fast) q_loop(BoolTag<true>());
@@ -557,8 +558,9 @@ __device__ __forceinline__ int cost_cut(const AdmitParams& p, const float* wg, c
 
 // Persistent CTA per SM (header comment). Shared memory: C_g u16 [c_stride] | S_g u16
 // [s_stride] | control (16 B) | blockDim/32 teams of team_smem bytes.
-template <int PK>
-__global__ void __launch_bounds__(1024, 1) admit_group_kernel(AdmitParams p) {
+// NT = the block size the register budget is sized for (64 K registers / NT per thread).
+template <int PK, int NT, bool EST>
+__global__ void __launch_bounds__(NT, 1) admit_group_kernel(AdmitParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint16_t* sC = reinterpret_cast<uint16_t*>(smem_raw);
   uint16_t* sS = sC + p.c_stride;
@@ -670,11 +672,15 @@ __global__ void __launch_bounds__(1024, 1) admit_group_kernel(AdmitParams p) {
         ctl[0] = s_lo;
         flush_cost();
         ctl[3] = g;
+        *seg_cnt = (uint32_t)(s_hi - s_lo);
       }
     }
     __syncthreads();
     const int64_t gid_base = (int64_t)g * p.members_per_group + p.member_base - __ldg(p.group_off + g);
     const uint32_t a_ctl = sh_addr(ctl);
+    // this warp's busy cycles in the segment (start kept in its team scratch, not a register)
+    uint32_t* t_start = reinterpret_cast<uint32_t*>(base + p.team_smem) - 1;
+    if (lane == 0) *t_start = (uint32_t)clock();
 #pragma unroll 1
     for (;;) {
       __syncwarp();  // the previous instance's shared-memory reads are done
@@ -682,13 +688,9 @@ __global__ void __launch_bounds__(1024, 1) admit_group_kernel(AdmitParams p) {
       if (lane == 0) i = (int)atom_add_sh(a_ctl, 1u);
       i = __shfl_sync(0xffffffffu, i, 0);
       if (i >= s_hi) break;
-      const uint32_t t0 = (uint32_t)clock();
-      group_one<PK>(p, lane, base, i, sC, sS, gid_base);
-      if (cost_wr && lane == 0) {
-        atom_add_sh(a_ctl + 16u, (uint32_t)clock() - t0);
-        atom_add_sh(a_ctl + 20u, 1u);
-      }
+      group_one<PK, EST>(p, lane, base, i, sC, sS, gid_base);
     }
+    if (cost_wr && lane == 0) atom_add_sh(a_ctl + 16u, (uint32_t)clock() - *t_start);
     s_lo = s_hi;
     ++g;
   }

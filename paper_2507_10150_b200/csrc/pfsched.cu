@@ -293,6 +293,17 @@ pf_status pf_nccl_unique_id(void* id_out) {
   return PF_OK;
 }
 
+// admit_group_kernel instance: packing (PK 9 / 10) x block size the registers are sized for
+// (1024: 64 registers; 768: 85) x estimate-only.
+static const void* group_fn(const pf_ctx* c, bool est) {
+  const bool wide = c->gp_warps > 24;
+#define PF_GFN(PK, NT) (est ? reinterpret_cast<const void*>(pf::admit_group_kernel<PK, NT, true>) \
+                            : reinterpret_cast<const void*>(pf::admit_group_kernel<PK, NT, false>))
+  if (c->pack == 1) return wide ? PF_GFN(9, 1024) : PF_GFN(9, 768);
+  return wide ? PF_GFN(10, 1024) : PF_GFN(10, 768);
+#undef PF_GFN
+}
+
 pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* stream,
                     pf_ctx** out) {
   if (!cfg || !out) return fail(PF_EINVAL, "pf_create: NULL cfg/out");
@@ -487,9 +498,13 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     if (nw >= 8 && !(ev && ev[0] == '0')) {
       c->gp_warps = nw;
       c->gp_smem = tables + (size_t)nw * team;
-      const void* gfn = c->pack == 1 ? reinterpret_cast<const void*>(pf::admit_group_kernel<9>)
-                                     : reinterpret_cast<const void*>(pf::admit_group_kernel<10>);
-      PF_CUDA_C(ensure_smem(gfn, (int)c->gp_smem));
+      const char* wv = getenv("PFSCHED_GROUP_WARPS");  // A/B knob: teams per CTA (≤ 32)
+      if (wv && atoi(wv) >= 8 && atoi(wv) < c->gp_warps) {
+        c->gp_warps = atoi(wv);
+        c->gp_smem = tables + (size_t)c->gp_warps * team;
+      }
+      PF_CUDA_C(ensure_smem(group_fn(c, false), (int)c->gp_smem));
+      PF_CUDA_C(ensure_smem(group_fn(c, true), (int)c->gp_smem));
       int dev = 0;
       PF_CUDA_C(cudaGetDevice(&dev));
       PF_CUDA_C(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
@@ -636,16 +651,13 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
   p.lhat_q = lhat_q;
   p.err = c->err;
   if (c->gp_warps && !lhat_run) {
-    const void* gfn = c->pack == 1 ? reinterpret_cast<const void*>(pf::admit_group_kernel<9>)
-                                   : reinterpret_cast<const void*>(pf::admit_group_kernel<10>);
-    PF_CUDA(ensure_smem(gfn, (int)c->gp_smem));
+    const bool est = (q_off == nullptr);
+    PF_CUDA(ensure_smem(group_fn(c, est), (int)c->gp_smem));
     const int grid = std::max(1, std::min(c->sms, C.n_instances));
     p.gcost = c->gcost;
     p.cost_epoch = c->cost_epoch++;
-    if (c->pack == 1)
-      pf::admit_group_kernel<9><<<grid, c->gp_warps * 32, c->gp_smem, s>>>(p);
-    else
-      pf::admit_group_kernel<10><<<grid, c->gp_warps * 32, c->gp_smem, s>>>(p);
+    void* args[] = {&p};
+    PF_CUDA(cudaLaunchKernel(group_fn(c, est), dim3(grid), dim3(c->gp_warps * 32), args, c->gp_smem, s));
     PF_CUDA(cudaGetLastError());
     return PF_OK;
   }
