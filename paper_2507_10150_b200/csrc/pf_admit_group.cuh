@@ -59,6 +59,17 @@ __device__ __forceinline__ uint32_t atom_add_sh(uint32_t a, uint32_t v) {
   return old;
 }
 
+// Bulk L2 prefetch (TMA) of n int32 elements from a (rounded out to 16-byte boundaries).
+#ifndef PF_AHEAD
+#define PF_AHEAD 32
+#endif
+__device__ __forceinline__ void prefetch_l2(const int32_t* a, int n) {
+  if (n <= 0) return;
+  const uint64_t lo = reinterpret_cast<uint64_t>(a) & ~uint64_t(15);
+  const uint64_t hi = (reinterpret_cast<uint64_t>(a + n) + 15) & ~uint64_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
+}
+
 __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t x;
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(a), "r"(b), "r"(c));
@@ -72,7 +83,7 @@ __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
 template <int PK, bool EST>
 __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, unsigned char* base,
                                           const int i, const uint16_t* sC, const uint16_t* sS,
-                                          const int64_t gid_base) {
+                                          const int64_t gid_base, const int* pf_ctl) {
   constexpr int NB = 128;
   constexpr int NSH = PK;
   constexpr uint32_t NMASK = (1u << NSH) - 1u;
@@ -113,6 +124,21 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
           for (int e = lane; e < q; e += 32) p.pred_q_out[q0 + e] = -1;
       }
       return;
+    }
+  }
+  // L2 prefetch of the request rows PF_AHEAD instances ahead in this CTA's stream (its range
+  // is contiguous in the CSR arrays): every instance prefetches about one instance's rows
+  // at (its own rows + PF_AHEAD mean-instance sizes), so the warps together keep the stream
+  // in L2 ahead of their loads (the first chunk of an instance otherwise waits a DRAM trip).
+  if (PF_AHEAD > 0 && lane == 0) {
+    const int d = pf_ctl[0], rend = pf_ctl[2];
+    const int a = ::min(r0 + d, rend), b = ::min(r1 + d, rend);
+    prefetch_l2(p.input_len + a, b - a);
+    prefetch_l2(p.generated + a, b - a);
+    if (!EST) {
+      const int dq = pf_ctl[1], qend = pf_ctl[3];
+      const int c = ::min(q0 + dq, qend), e = ::min(q1 + dq, qend);
+      prefetch_l2(p.q_input_len + c, e - c);
     }
   }
   // C = ⌊(10^4 − bp)·cap / 10^4⌋ in 32-bit arithmetic (C-12, C-13): cap = 10^4·Q + R gives
@@ -565,12 +591,14 @@ __global__ void __launch_bounds__(NT, 1) admit_group_kernel(AdmitParams p) {
   uint16_t* sC = reinterpret_cast<uint16_t*>(smem_raw);
   uint16_t* sS = sC + p.c_stride;
   // control: [0] next instance, [1] lo, [2] hi, [3] group of the open cost segment,
-  // [4] SM cycles (u32: < 2^32 per CTA segment) and [5] instances of that segment
+  // [4] SM cycles (u32: < 2^32 per CTA segment) and [5] instances of that segment,
+  // [8..11] the segment's L2 prefetch stream: mean running / queued rows per instance
+  // times PF_AHEAD, and the end of its running / queued rows
   int* ctl = reinterpret_cast<int*>(sS + p.s_stride);
   unsigned int* seg_cyc = reinterpret_cast<unsigned int*>(ctl + 4);
   unsigned int* seg_cnt = reinterpret_cast<unsigned int*>(ctl + 5);
   const int lane = threadIdx.x & 31;
-  unsigned char* base = reinterpret_cast<unsigned char*>(ctl + 8) + (size_t)(threadIdx.x >> 5) * p.team_smem;
+  unsigned char* base = reinterpret_cast<unsigned char*>(ctl + 16) + (size_t)(threadIdx.x >> 5) * p.team_smem;
   const int G = p.n_groups;
   unsigned long long* cost_wr = p.gcost ? p.gcost + (size_t)(p.cost_epoch % 3) * 2 * G : nullptr;
   if (p.gcost && blockIdx.x == 0) {  // zero the buffer the next launch adds to
@@ -673,6 +701,14 @@ __global__ void __launch_bounds__(NT, 1) admit_group_kernel(AdmitParams p) {
         flush_cost();
         ctl[3] = g;
         *seg_cnt = (uint32_t)(s_hi - s_lo);
+        const int rlo = __ldg(p.run_off + s_lo), rhi = __ldg(p.run_off + s_hi);
+        ctl[8] = (int)(((int64_t)(rhi - rlo) * PF_AHEAD) / (s_hi - s_lo));
+        ctl[10] = rhi;
+        if (!EST) {
+          const int qlo = __ldg(p.q_off + s_lo), qhi = __ldg(p.q_off + s_hi);
+          ctl[9] = (int)(((int64_t)(qhi - qlo) * PF_AHEAD) / (s_hi - s_lo));
+          ctl[11] = qhi;
+        }
       }
     }
     __syncthreads();
@@ -688,7 +724,7 @@ __global__ void __launch_bounds__(NT, 1) admit_group_kernel(AdmitParams p) {
       if (lane == 0) i = (int)atom_add_sh(a_ctl, 1u);
       i = __shfl_sync(0xffffffffu, i, 0);
       if (i >= s_hi) break;
-      group_one<PK, EST>(p, lane, base, i, sC, sS, gid_base);
+      group_one<PK, EST>(p, lane, base, i, sC, sS, gid_base, ctl + 8);
     }
     if (cost_wr && lane == 0) atom_add_sh(a_ctl + 16u, (uint32_t)clock() - *t_start);
     s_lo = s_hi;

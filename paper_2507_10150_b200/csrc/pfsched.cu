@@ -492,7 +492,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   // PFSCHED_GROUP_KERNEL=0 selects the cached-table admit_kernel instead (A/B measurements).
   if (c->layout == LAYOUT_GROUP && V.TW == 1 && c->pack != 0) {
     const char* ev = getenv("PFSCHED_GROUP_KERNEL");
-    const size_t tables = (size_t)(c->c_stride + c->s_stride) * 2 + 32;
+    const size_t tables = (size_t)(c->c_stride + c->s_stride) * 2 + 64;
     const size_t avail = 232448;  // 227 KB opt-in maximum per block
     const int nw = avail > tables ? (int)std::min<size_t>(32, (avail - tables) / team) : 0;
     if (nw >= 8 && !(ev && ev[0] == '0')) {
