@@ -312,7 +312,7 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   // Lane t owns bins [4t, 4t+4) (descending r). Packed prefix words P = A << NSH | N never
   // carry (host PK bound), so R and R ∪ Q' are two running packed sums.
   const int b0 = lane * 4;
-  auto evaluate = [&](int qlim, bool first) -> Eval {
+  auto evaluate = [&](int qlim, bool first) -> Eval {  // first: also M*(R)
     const uint4 e4 = __ldg(reinterpret_cast<const uint4*>(p.edges + b0));  // lo | hi << 16 (L1)
     const uint32_t ed[4] = {e4.x, e4.y, e4.z, e4.w};
     const uint4 r4 = *reinterpret_cast<const uint4*>(binR + b0);
@@ -335,23 +335,23 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       vT = iT - vT;
     }
     const uint32_t s0R = vR, s0T = vT;  // packed sums over the bins before this lane's
-    int lb_r = 0, lb_a = 0, bx = 0, ub_r = 0, ub_a = 0;
+    int lb_r = 0, lb_a = 0, bx = 0, ub_r = 0;
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
-      vR += rr[x];
       vT += rr[x] + qq[x];
-      const int AR = (int)(vR >> NSH), NR = (int)(vR & NMASK);
       const int A = (int)(vT >> NSH), N = (int)(vT & NMASK);
       const int lo = (int)(ed[x] & 0xFFFF), hi = (int)(ed[x] >> 16);
-      if (first) lb_r = ::max(lb_r, AR + lo * NR);  // exact T_R(lo)
-      const int va = A + lo * N;                    // exact T_{R∪Q'}(lo)
+      if (first) {
+        vR += rr[x];
+        const int AR = (int)(vR >> NSH), NR = (int)(vR & NMASK);
+        lb_r = ::max(lb_r, AR + lo * NR);  // exact T_R(lo)
+        // wide bin holding running requests: upper bound of T_R on its range
+        ub_r = ::max(ub_r, (hi > lo && (rr[x] & NMASK)) ? AR + hi * NR : 0);
+      }
+      const int va = A + lo * N;  // exact T_{R∪Q'}(lo)
       if (va > lb_a) {
         lb_a = va;
         bx = x;
-      }
-      if (hi > lo) {  // wide bin: upper bounds where it holds requests
-        if (first && (rr[x] & NMASK)) ub_r = ::max(ub_r, AR + hi * NR);
-        if ((rr[x] + qq[x]) & NMASK) ub_a = ::max(ub_a, A + hi * N);
       }
     }
     Eval ev;
@@ -372,7 +372,21 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       ev.t_run = __shfl_sync(0xffffffffu, trun, who);
     }
     const bool need_r = first && __reduce_max_sync(0xffffffffu, ub_r) > ev.m_run;
-    const bool need_a = !estimate_only && ev.m_all <= Cmax && __reduce_max_sync(0xffffffffu, ub_a) > ev.m_all;
+    // M*(R ∪ Q') must be exact only when it can be the reported peak (≤ C); above C the bin
+    // attaining the largest exact lower bound already gives a violating τ. Only then are
+    // the upper bounds of the wide bins holding requests needed (a second walk).
+    bool need_a = false;
+    if (!estimate_only && ev.m_all <= Cmax) {
+      uint32_t v = s0T;
+      int ub_a = 0;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        v += rr[x] + qq[x];
+        const int lo = (int)(ed[x] & 0xFFFF), hi = (int)(ed[x] >> 16);
+        ub_a = ::max(ub_a, (hi > lo && ((rr[x] + qq[x]) & NMASK)) ? (int)(v >> NSH) + hi * (int)(v & NMASK) : 0);
+      }
+      need_a = __reduce_max_sync(0xffffffffu, ub_a) > ev.m_all;
+    }
     if (!need_r && !need_a) return ev;
     // ---- refinement of the wide bins whose upper bound beats the current maximum
     if (lane == 0) cand[0] = 0;
@@ -494,6 +508,8 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   };
 
   // ---- a7: Alg.1 lines 7-14 — exact p* by cutting planes (pf_admit.cuh header).
+  // (one call site of the evaluation: a second inlined copy costs more in instruction-cache
+  // misses than its specialisation saves, measured +12 %)
   int p_star = 0, peak = 0, M0 = 0, ph = q;
   bool first = true;
 #pragma unroll 1
