@@ -245,20 +245,12 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       for (; e0 + 4 * 32 <= k; e0 += 4 * 32)
         chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<true>(), fast_tag,
               IntTag<4>(), BoolTag<true>());
-      // ragged tail (< 128 requests): 2-, 1- and one predicated 1-request-per-lane chunks
-      if (e0 + 2 * 32 <= k) {
-        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<true>(), fast_tag,
-              IntTag<2>(), BoolTag<true>());
-        e0 += 2 * 32;
-      }
-      if (e0 + 32 <= k) {
-        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<true>(), fast_tag,
-              IntTag<1>(), BoolTag<true>());
-        e0 += 32;
-      }
-      if (e0 < k)
-        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<false>(), fast_tag,
-              IntTag<1>(), BoolTag<true>());
+      // ragged tail (< 128 requests): predicated 1-request-per-lane chunks (one code copy:
+      // fewer hot instructions for the instruction cache than 2-/1-request variants)
+#pragma unroll 1
+      for (; e0 < k; e0 += 32)
+        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<false>(), fast_tag, IntTag<1>(),
+              BoolTag<true>());
     };
     if (draw_fast) run_loop(BoolTag<true>());
     else run_loop(BoolTag<false>());
@@ -272,14 +264,10 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       for (; j0 + 2 * 32 <= q; j0 += 2 * 32)
         chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<true>(), fast_tag,
               IntTag<2>(), BoolTag<false>());
-      if (j0 + 32 <= q) {
-        chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<true>(), fast_tag,
-              IntTag<1>(), BoolTag<false>());
-        j0 += 32;
-      }
-      if (j0 < q)
-        chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<false>(), fast_tag,
-              IntTag<1>(), BoolTag<false>());
+#pragma unroll 1
+      for (; j0 < q; j0 += 32)
+        chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<false>(), fast_tag, IntTag<1>(),
+              BoolTag<false>());
     };
     if (draw_fast) q_loop(BoolTag<true>());
     else q_loop(BoolTag<false>());
