@@ -70,6 +70,19 @@ __device__ __forceinline__ void prefetch_l2(const int32_t* a, int n) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
 }
 
+// One inclusive-scan step: v += (value of lane − d) when that lane exists (the shuffle's own
+// in-range predicate guards the add: no lane compare, no select).
+__device__ __forceinline__ uint32_t scan_step(uint32_t v, int d) {
+  asm volatile("{\n .reg .pred p;\n .reg .b32 t;\n shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n"
+               " @p add.u32 %0, %0, t;\n}" : "+r"(v) : "r"(d));
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_incl_u32(uint32_t v) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) v = scan_step(v, d);
+  return v;
+}
+
 __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t x;
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(a), "r"(b), "r"(c));
@@ -312,12 +325,8 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       uint32_t iR = vR, iT = vT;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t tR = __shfl_up_sync(0xffffffffu, iR, d);
-        const uint32_t tT = __shfl_up_sync(0xffffffffu, iT, d);
-        if (lane >= d) {
-          iR += tR;
-          iT += tT;
-        }
+        iR = scan_step(iR, d);
+        iT = scan_step(iT, d);
       }
       vR = iR - vR;
       vT = iT - vT;
@@ -537,7 +546,7 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
         const uint32_t rec = rb[k + jx];
         wv = ((int)(rec & 0x1FFFu) >= tau) ? (int)(rec >> 13) + tau : 0;
       }
-      const int inc = warp_inclusive_add(wv, lane);
+      const int inc = (int)warp_incl_u32((uint32_t)wv);
       if (jx < ph && carry + inc > Cmax) first_bad = ::min(first_bad, jx + 1);
       carry += __shfl_sync(0xffffffffu, inc, 31);
       if (__any_sync(0xffffffffu, first_bad != 0x7FFFFFFF)) break;
