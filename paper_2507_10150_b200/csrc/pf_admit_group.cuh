@@ -187,7 +187,9 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   // ragged tail chunk predicates its loads (0 when out of range), stores and atomics.
   // Queued requests (slot k + j) have l_t = 0, so b = C_g[0] (= 0: history lengths ≥ 1)
   // is one shared value and the prediction is one lookup.
-  bool my_bad = false;
+  // validation by running maxima of the unsigned inputs (negative values wrap above any
+  // bound): bad iff max l_p > max_input_len or max l_t ≥ max_new (one VIMNMX per input)
+  uint32_t mx_lp = 0, mx_lt = 0;
   const uint32_t mx1 = (uint32_t)(max_new - 1);
   const uint32_t bq0 = sC[0];
   const uint32_t a_rb = sh_addr(rb), a_nx = sh_addr(nx), a_hd = sh_addr(hd);
@@ -212,10 +214,11 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       const int e = (RUN ? 0 : k) + e0 + c * 32 + lane;  // slot
       // l_p ∉ [0, max_input_len] or l_t ∉ [0, max_new) (unsigned compares catch < 0)
       if (RUN) {
-        my_bad |= ((uint32_t)lp[c] > lpmax) | ((uint32_t)lt[c] > mx1);
+        mx_lp = ::max(mx_lp, (uint32_t)lp[c]);
+        mx_lt = ::max(mx_lt, (uint32_t)lt[c]);
         lt[c] = (int)::min((uint32_t)lt[c], mx1);  // keeps the lookups in range
       } else {
-        my_bad |= (uint32_t)lp[c] > lpmax;
+        mx_lp = ::max(mx_lp, (uint32_t)lp[c]);
       }
       const uint32_t u = FAST ? lowbias32(key_fold ^ ((uint32_t)e * 0x9E3779B9U))
                               : draw_slow(p, key_fold, e, R);
@@ -285,7 +288,7 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
     if (draw_fast) q_loop(BoolTag<true>());
     else q_loop(BoolTag<false>());
   }
-  if (__any_sync(0xffffffffu, my_bad)) {
+  if (__any_sync(0xffffffffu, (mx_lp > lpmax) | (mx_lt > mx1))) {
     // Data-dependent violation: outputs of this instance are −1.
     for (int e = lane; e < n_ent; e += 32) {
       const int l_p = e < k ? p.input_len[r0 + e] : p.q_input_len[q0 + (e - k)];
