@@ -622,7 +622,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                          "frac": achieved / peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": abytes, "kernel": "admit_kernel",
+                         "algorithmic_bytes_per_launch": abytes,
+                         "kernel": "admit_group_kernel" if (cfg.shared and os.environ.get("PFSCHED_GROUP_KERNEL", "1") != "0")
+                         else "admit_kernel",
                          "frac_of_8TBs_spec": achieved / 8000.0, "issue": issue},
             "e2e": {"value": e2e_value, "unit": UNIT, "pipelined": "step t+1's H2D overlaps step t",
                     "h2d_bytes_per_step": int(h2d + h2d_c),

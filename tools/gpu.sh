@@ -38,12 +38,12 @@ case "$mode" in
     echo "reference=$?" ;;
   launches)
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
-      -k regex:"admit_kernel|group_tables|update_hist|update_sorted|init_ring|hist_rows|sort_rows" \
+      -k regex:"admit_kernel|admit_group_kernel|group_tables|update_hist|update_sorted|init_ring|hist_rows|sort_rows" \
       python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo "launches=$?" ;;
   ncu)
     c=${1:-5}; tag=${2:-admit_cfg$c}
-    timeout 600 ncu --set full --import-source on --clock-control none -k regex:admit_kernel -c 1 -o "gpurun_out/$tag" \
-      python tools/prof_admit.py --config "$c" --ticks 2 > "gpurun_out/$tag.log" 2>&1; echo "ncu=$?" ;;
+    timeout 600 ncu --set full --import-source on --clock-control none -k regex:admit --launch-skip 3 -c 1 -o "gpurun_out/$tag" \
+      python tools/prof_admit.py --config "$c" --ticks 4 > "gpurun_out/$tag.log" 2>&1; echo "ncu=$?" ;;
   ab)
     bash tools/ab.sh "$1" "${2:-5}" ;;
   parity)

@@ -5,7 +5,7 @@ import collections
 import csv
 import sys
 
-OURS = ("admit_kernel", "update_hist_kernel", "update_sorted_kernel", "group_tables_kernel",
+OURS = ("admit_kernel", "admit_group_kernel", "update_hist_kernel", "update_sorted_kernel", "group_tables_kernel",
         "init_ring_kernel", "hist_rows_kernel", "sort_rows_kernel", "baseline_kernel", "sim_",
         "gram_kernel", "adjacent_kernel", "cosine_kernel")
 path, cmd = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else ""
@@ -28,7 +28,7 @@ print(" compare SHARES, not absolutes; only this library's kernels are listed)\n
 for k, v in t.items():
     print(f"{len(v):4d} launches  mean {sum(v) / len(v):9.1f} us  min {min(v):9.1f}  max {max(v):9.1f}  {k[:110]}")
 mean = {k: sum(v) / len(v) for k, v in t.items()}
-step = {"admit": sum(m for k, m in mean.items() if "admit_kernel" in k),
+step = {"admit": sum(m for k, m in mean.items() if "admit" in k),
         "update_history": sum(m for k, m in mean.items() if "update_" in k),
         "group_tables": sum(m for k, m in mean.items() if "group_tables" in k)}
 tot = sum(step.values())
