@@ -357,13 +357,15 @@ __device__ __forceinline__ void admit_one(const AdmitParams& p, Team<TW>& T, uns
   constexpr int NB = 32 * BPT * TW;
   // PK = bits of the N field of a packed bin word (A << PK | N); 0 = unpacked bins and
   // records. 9: N < 512 (max_entries < 512); 10: N < 1024 with Σ a < 2^22 (host bound).
-  constexpr bool PACK = PK != 0;
-  constexpr int NSH = PK ? PK : 9;
+  // PK = 1: packed records (r | a << 13) with unpacked bins (k + q ≥ 1024 or large Σ a)
+  constexpr bool RP = PK != 0;    // packed request records
+  constexpr bool PACK = PK >= 9;  // packed bin words
+  constexpr int NSH = PACK ? PK : 9;
   constexpr uint32_t NMASK = (1u << NSH) - 1u;
   constexpr int NBW = PACK ? NB : 2 * NB;
   uint32_t* rb = reinterpret_cast<uint32_t*>(base);
-  int* av = reinterpret_cast<int*>(rb + p.ent_cap);  // unused when PACK
-  uint16_t* nx = reinterpret_cast<uint16_t*>(av + (PACK ? 0 : p.ent_cap));
+  int* av = reinterpret_cast<int*>(rb + p.ent_cap);  // unused when RP
+  uint16_t* nx = reinterpret_cast<uint16_t*>(av + (RP ? 0 : p.ent_cap));
   uint32_t* hd = reinterpret_cast<uint32_t*>(nx + p.ent_cap);
   uint32_t* rmn = hd + NB;                 // [NB] min r per bin (PF_MINMAX)
   uint32_t* rmx = rmn + (MinMax<TW>::on ? NB : 0);  // [NB] max r per bin
@@ -371,8 +373,8 @@ __device__ __forceinline__ void admit_one(const AdmitParams& p, Team<TW>& T, uns
   uint32_t* binQ = binR + NBW;
   T.xs = reinterpret_cast<int*>(binQ + NBW);
   int* cand = T.xs + 40;    // [0]: count, then 6 ints per candidate (≤ 16); xs[36]: list size
-  auto ent_r = [&](int e) -> int { return (int)(rb[e] & (PACK ? 0x1FFFu : 0xFFFFu)); };
-  auto ent_a = [&](int e) -> int { return PACK ? (int)(rb[e] >> 13) : av[e]; };
+  auto ent_r = [&](int e) -> int { return (int)(rb[e] & (RP ? 0x1FFFu : 0xFFFFu)); };
+  auto ent_a = [&](int e) -> int { return RP ? (int)(rb[e] >> 13) : av[e]; };
   int32_t* table = T.xs + 140;
   uint16_t* tS = reinterpret_cast<uint16_t*>(table);  // LOOK_SORTED: the window, u16 (Lmax < 2^16)
 
@@ -532,7 +534,7 @@ __device__ __forceinline__ void admit_one(const AdmitParams& p, Team<TW>& T, uns
     const int r = l_hat - l_t;  // ≥ 1 (C-4)
     const int a = l_p + l_t;
     const int b = bin_of<NB>(r);
-    if (PACK) {
+    if (RP) {
       rb[e] = (uint32_t)r | ((uint32_t)a << 13);
     } else {
       rb[e] = (uint32_t)r | ((uint32_t)b << 16);
@@ -1025,7 +1027,7 @@ __device__ __forceinline__ void admit_one(const AdmitParams& p, Team<TW>& T, uns
     }
     T.sync();
     for (int jx = tid; jx < ph; jx += TT) {
-      const int b = PACK ? bin_of<NB>(ent_r(k + jx)) : (int)(rb[k + jx] >> 16);
+      const int b = RP ? bin_of<NB>(ent_r(k + jx)) : (int)(rb[k + jx] >> 16);
       const int a = ent_a(k + jx);
       if (PACK) {
         atomicAdd(&binQ[b], ((uint32_t)a << NSH) | 1u);

@@ -60,10 +60,11 @@ enum Layout { LAYOUT_SORTED = 0, LAYOUT_HIST = 1, LAYOUT_GROUP = 2 };
 typedef void (*AdmitFn)(pf::AdmitParams);
 struct Variant {
   int TW, cap;       // team warps, max requests per instance served
-  AdmitFn fn[3][3];  // [lookup][pack]
+  AdmitFn fn[3][4];  // [lookup][pack]
 };
 // pack index 0: unpacked; 1: A << 9 | N bins (requires max_entries < 512, so one-warp
-// teams only); 2: A << 10 | N bins (one-warp teams only). Variants that can never be
+// teams only); 2: A << 10 | N bins (one-warp teams only); 3: packed records r | a << 13
+// with unpacked bins (PK = 1: e.g. config 4's 1280 requests per instance). Variants that can never be
 // selected are not instantiated.
 template <int TW, int LOOK, int PK>
 AdmitFn packed_variant() {
@@ -73,11 +74,11 @@ AdmitFn packed_variant() {
 #define PF_VARIANT(TW, CAP)                                                                    \
   {TW, CAP,                                                                                   \
    {{pf::admit_kernel<TW, pf::LOOK_SORTED, 0>, packed_variant<TW, pf::LOOK_SORTED, 9>(),       \
-     packed_variant<TW, pf::LOOK_SORTED, 10>()},                                              \
+     packed_variant<TW, pf::LOOK_SORTED, 10>(), pf::admit_kernel<TW, pf::LOOK_SORTED, 1>},    \
     {pf::admit_kernel<TW, pf::LOOK_HIST, 0>, packed_variant<TW, pf::LOOK_HIST, 9>(),           \
-     packed_variant<TW, pf::LOOK_HIST, 10>()},                                                \
+     packed_variant<TW, pf::LOOK_HIST, 10>(), pf::admit_kernel<TW, pf::LOOK_HIST, 1>},        \
     {pf::admit_kernel<TW, pf::LOOK_GROUP, 0>, packed_variant<TW, pf::LOOK_GROUP, 9>(),         \
-     packed_variant<TW, pf::LOOK_GROUP, 10>()}}}
+     packed_variant<TW, pf::LOOK_GROUP, 10>(), pf::admit_kernel<TW, pf::LOOK_GROUP, 1>}}}
 const Variant kVariants[] = {PF_VARIANT(1, 512), PF_VARIANT(2, 1024), PF_VARIANT(4, 2048),
                              PF_VARIANT(8, 4096)};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
@@ -461,6 +462,8 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
       c->pack = 1;
     else if (rec && V.TW == 1 && C.max_entries < 1024 && (int64_t)C.max_entries * amax < (1LL << 22))
       c->pack = 2;
+    else if (rec)
+      c->pack = 3;  // records packed (4 B per request instead of 8 in shared memory)
     else
       c->pack = 0;
   }
@@ -472,7 +475,8 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
     table = (size_t)((C.window + 2) & ~1) * 2 + (size_t)((1 << c->cbits) + 2) * 2;
   if (c->layout == LAYOUT_HIST) table = (size_t)nb * 4;
   c->ent_cap = (C.max_entries + 7) & ~7;
-  const size_t nbw = (size_t)c->n_bins * (c->pack ? 1 : 2);
+  const bool bins_packed = c->pack == 1 || c->pack == 2;
+  const size_t nbw = (size_t)c->n_bins * (bins_packed ? 1 : 2);
   size_t team = (size_t)c->ent_cap * (c->pack ? 6 : 10) + (size_t)c->n_bins * 4 * ((PF_MINMAX && V.TW > 1) ? 3 : 1) +
                 nbw * 8 + 140 * 4 + table;
   team = (team + 15) & ~(size_t)15;
@@ -490,7 +494,7 @@ pf_status pf_create(const pf_config* cfg, const int32_t* init_history, void* str
   // Shared mode, one-warp teams, packed bins: the persistent admit_group_kernel with the
   // group tables in shared memory (pf_admit.cuh), when the tables leave room for ≥ 8 teams.
   // PFSCHED_GROUP_KERNEL=0 selects the cached-table admit_kernel instead (A/B measurements).
-  if (c->layout == LAYOUT_GROUP && V.TW == 1 && c->pack != 0) {
+  if (c->layout == LAYOUT_GROUP && V.TW == 1 && bins_packed) {
     const char* ev = getenv("PFSCHED_GROUP_KERNEL");
     const size_t tables = (size_t)(c->c_stride + c->s_stride) * 2 + 64;
     const size_t avail = 232448;  // 227 KB opt-in maximum per block
