@@ -13,6 +13,7 @@
 #   bash tools/gpu.sh sanitize          compute-sanitizer memcheck / racecheck / synccheck over GPU parity cases
 #   bash tools/gpu.sh profile TAG [C]   ncu --set full of the 4th admit launch of config C (default 5) + raw / SASS csv
 #                                       (read here with tools/ncu_keys.py, tools/sass_hist.py, tools/sass_blocks.py)
+#   bash tools/gpu.sh final             tests, bench lines, oracle arm, launch list, ncu cfg 5/4, shard probe
 #   bash tools/gpu.sh groupab           bench cfg 5 with admit_group_kernel (default) and with admit_kernel
 #                                       (PFSCHED_GROUP_KERNEL=0) on one box
 #
@@ -72,5 +73,16 @@ case "$mode" in
       PFSCHED_GROUP_KERNEL=$v timeout 300 python bench.py --no-cpu-baseline --e2e-steps 1 --steps 100 --warmup 5 2>/dev/null \
         | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('group_kernel=$v', 'admit_ms', round(d['config']['admit_kernel_ms'], 4), 'step_ms', round(d['ms_per_step'], 4), d['config']['output_check'])"
     done ;;
+  final)
+    # the round-end evidence set: tests + smoke, bench lines cfg 5 (default) and 1-4, the oracle
+    # arm, the launch list, ncu of the cfg 5 and cfg 4 admit kernels, the P-rank shard probe
+    bash tools/gpu.sh tests
+    bash tools/gpu.sh bench 1 2 3 4
+    bash tools/gpu.sh reference
+    bash tools/gpu.sh launches
+    python tools/ncu_launches.py gpurun_out/launches_bench.csv "bench.py --steps 4 --warmup 3" > gpurun_out/launches_summary.txt 2>&1
+    bash tools/gpu.sh profile final_cfg5 5
+    bash tools/gpu.sh profile final_cfg4 4
+    timeout 600 python tools/shard_probe.py > gpurun_out/shard_probe.txt 2>&1; echo "probe=$?" ;;
   *) echo "unknown mode $mode"; exit 2 ;;
 esac
