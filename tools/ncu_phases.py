@@ -7,7 +7,7 @@ inlined helpers (pf_common.cuh hash / scans, the Team primitives, CUDA intrinsic
 inherit the phase of the nearest preceding body instruction in address order (the compiler
 lays the inlined code out at its call site).
 
-Usage: python tools/ncu_phases.py report.ncu-rep N_INSTANCES [--src pf_admit.cuh]"""
+Usage: python tools/ncu_phases.py report.ncu-rep N_INSTANCES [--src pf_admit.cuh | --group]"""
 import csv
 import os
 import re
@@ -26,11 +26,24 @@ MARKERS = [  # (regex of the first line of a section, phase)
 ]
 
 
+# admit_group_kernel (pf_admit_group.cuh): --group
+GROUP_SRC = os.path.join(ROOT, "paper_2507_10150_b200", "csrc", "pf_admit_group.cuh")
+GROUP_MARKERS = [
+    (r"^__device__ __forceinline__ void group_one\(", "prologue (scalars, validation, prefetch, key)"),
+    (r"// ---- a4 \(Alg.1 l.3-9\)", "a4 predict (loads, hash, lookups, binning)"),
+    (r"if \(__any_sync\(0xffffffffu, \(mx_lp > lpmax\)", "prologue (scalars, validation, prefetch, key)"),
+    (r"auto evaluate = ", "a5/a6 evaluation (bins, scans, bounds)"),
+    (r"// ---- refinement of the wide bins", "a5/a6 refinement (list walks)"),
+    (r"// ---- a7: Alg.1 lines 7-14", "a7 cutting plane (p_max scan, binQ rebuild)"),
+    (r"^// Cost-weighted partition", "kernel loop (partition, segments, instance counter)"),
+]
+
+
 def sections(src=SRC):
     lines = open(src).read().splitlines()
     out = []
     for i, l in enumerate(lines, 1):
-        for rx, ph in MARKERS:
+        for rx, ph in (GROUP_MARKERS if src == GROUP_SRC else MARKERS):
             if re.search(rx, l):
                 out.append((i, ph))
     end = next(i for i, l in enumerate(lines, 1) if l.startswith("}  // namespace pf"))
@@ -48,7 +61,10 @@ def phase_of(line, secs, end):
 def main():
     rep, n = sys.argv[1], int(sys.argv[2])
     # --src FILE: the pf_admit.cuh the report was built from (e.g. an older commit's)
-    secs, end = sections(sys.argv[sys.argv.index("--src") + 1] if "--src" in sys.argv else SRC)
+    src = GROUP_SRC if "--group" in sys.argv else (
+        sys.argv[sys.argv.index("--src") + 1] if "--src" in sys.argv else SRC)
+    secs, end = sections(src)
+    base = os.path.basename(src)
     first = secs[0][0]
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
@@ -77,7 +93,7 @@ def main():
     ins.sort()
     agg, last = {}, "prologue (scalars, validation, tables, key)"
     for addr, (f, line), cnt in ins:
-        ph = phase_of(line, secs, end) if (f == "pf_admit.cuh" and line >= first) else None
+        ph = phase_of(line, secs, end) if (f == base and line >= first) else None
         if ph is None:
             ph = last
         else:
