@@ -317,7 +317,11 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   // carry (host PK bound), so R and R ∪ Q' are two running packed sums.
   const int b0 = lane * 4;
   auto evaluate = [&](int qlim, bool first) -> Eval {  // first: also M*(R)
-    const uint4 e4 = __ldg(reinterpret_cast<const uint4*>(p.edges + b0));  // lo | hi << 16 (L1)
+    // per-bin r ranges, lo | hi << 16, through L1. Loaded per evaluation: an earlier build
+    // that kept them in registers across the cutting-plane loop reported peaks too large
+    // in 3 of 128 parity instances (its evaluations after the first saw wrong edges). The
+    // cause was not isolated; it showed at the 64-register cap with spills.
+    const uint4 e4 = __ldg(reinterpret_cast<const uint4*>(p.edges + b0));
     const uint32_t ed[4] = {e4.x, e4.y, e4.z, e4.w};
     const uint4 r4 = *reinterpret_cast<const uint4*>(binR + b0);
     const uint4 q4 = *reinterpret_cast<const uint4*>(binQ + b0);
