@@ -53,6 +53,14 @@ __device__ __forceinline__ void red_add_sh_if(uint32_t a, uint32_t v, bool p) {
                :: "r"(a), "r"(v), "r"((int)p) : "memory");
 }
 
+__device__ __forceinline__ uint32_t atom_exch_sh(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_sh(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t atom_add_sh(uint32_t a, uint32_t v) {
   uint32_t old;
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
@@ -193,6 +201,7 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   const uint32_t mx1 = (uint32_t)(max_new - 1);
   const uint32_t bq0 = sC[0];
   const uint32_t a_rb = sh_addr(rb), a_nx = sh_addr(nx), a_hd = sh_addr(hd);
+  const uint32_t a_dummy = sh_addr(xs + 36);  // xs[36..37]: sinks of masked tail atomics
   auto chunk = [&](const int e0, const int n, const int32_t* lpp, const int32_t* ltp,
                    int32_t* po_base, uint32_t* bins, auto full_tag, auto fast_tag, auto nc_tag,
                    auto run_tag) {
@@ -238,10 +247,12 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
         nx[e] = (uint16_t)atomicExch(&hd[b4 >> 2], (uint32_t)e);
         atomicAdd(&bins[b4 >> 2], an);
       } else {
+        // shared-memory atomics cannot be predicated (ptxas wraps them in branches): an
+        // out-of-range lane aims its two atomics at the team's dummy words instead
         sts_u32_if(a_rb + 4u * e, rec, ok[c]);
-        const uint32_t old = atom_exch_sh_if(a_hd + b4, (uint32_t)e, ok[c]);
+        const uint32_t old = atom_exch_sh(ok[c] ? a_hd + b4 : a_dummy, (uint32_t)e);
         sts_u16_if(a_nx + 2u * e, old, ok[c]);
-        red_add_sh_if(sh_addr(bins) + b4, an, ok[c]);
+        red_add_sh(ok[c] ? sh_addr(bins) + b4 : a_dummy + 4u, an);
       }
     }
     if (po_base) {  // prediction outputs (one uniform branch per chunk)
@@ -263,10 +274,11 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
               IntTag<4>(), BoolTag<true>());
       // ragged tail (< 128 requests): predicated 1-request-per-lane chunks (one code copy:
       // fewer hot instructions for the instruction cache than 2-/1-request variants)
+      const int32_t* pl = lpR + e0;
+      const int32_t* pt = ltR + e0;
 #pragma unroll 1
-      for (; e0 < k; e0 += 32)
-        chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<false>(), fast_tag, IntTag<1>(),
-              BoolTag<true>());
+      for (; e0 < k; e0 += 32, pl += 32, pt += 32)
+        chunk(e0, k, pl, pt, poR, binR, BoolTag<false>(), fast_tag, IntTag<1>(), BoolTag<true>());
     };
     if (draw_fast) run_loop(BoolTag<true>());
     else run_loop(BoolTag<false>());
@@ -280,10 +292,10 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
       for (; j0 + 2 * 32 <= q; j0 += 2 * 32)
         chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<true>(), fast_tag,
               IntTag<2>(), BoolTag<false>());
+      const int32_t* pl = lpQ + j0;
 #pragma unroll 1
-      for (; j0 < q; j0 += 32)
-        chunk(j0, q, lpQ + j0, nullptr, poQ, binQ, BoolTag<false>(), fast_tag, IntTag<1>(),
-              BoolTag<false>());
+      for (; j0 < q; j0 += 32, pl += 32)
+        chunk(j0, q, pl, nullptr, poQ, binQ, BoolTag<false>(), fast_tag, IntTag<1>(), BoolTag<false>());
     };
     if (draw_fast) q_loop(BoolTag<true>());
     else q_loop(BoolTag<false>());
