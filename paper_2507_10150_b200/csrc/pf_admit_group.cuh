@@ -201,7 +201,9 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
   const uint32_t mx1 = (uint32_t)(max_new - 1);
   const uint32_t bq0 = sC[0];
   const uint32_t a_rb = sh_addr(rb), a_nx = sh_addr(nx), a_hd = sh_addr(hd);
-  const uint32_t a_dummy = sh_addr(xs + 36);  // xs[36..37]: sinks of masked tail atomics
+  // xs[lane]: this lane's sink for masked tail atomics (one word per lane, so masked lanes
+  // never serialise on one address)
+  const uint32_t a_dummy = sh_addr(xs + lane);
   auto chunk = [&](const int e0, const int n, const int32_t* lpp, const int32_t* ltp,
                    int32_t* po_base, uint32_t* bins, auto full_tag, auto fast_tag, auto nc_tag,
                    auto run_tag) {
@@ -252,7 +254,7 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
         sts_u32_if(a_rb + 4u * e, rec, ok[c]);
         const uint32_t old = atom_exch_sh(ok[c] ? a_hd + b4 : a_dummy, (uint32_t)e);
         sts_u16_if(a_nx + 2u * e, old, ok[c]);
-        red_add_sh(ok[c] ? sh_addr(bins) + b4 : a_dummy + 4u, an);
+        red_add_sh(ok[c] ? sh_addr(bins) + b4 : a_dummy, an);
       }
     }
     if (po_base) {  // prediction outputs (one uniform branch per chunk)
