@@ -19,6 +19,11 @@
 
 namespace pf {
 
+// Running requests per lane per full chunk.
+#ifndef PF_GNC
+#define PF_GNC 4
+#endif
+
 // Non-inlined slow draw (quantile mode or R ≠ 1; C-8/C-9), kept out of the hot loop's code.
 __device__ __noinline__ uint32_t draw_slow(const AdmitParams& p, uint32_t key_fold, int e, int R) {
   return (p.mode != 0) ? p.quantile_u : draw_u(key_fold, e, R);
@@ -271,9 +276,9 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
     auto run_loop = [&](auto fast_tag) {
       int e0 = 0;
 #pragma unroll 1
-      for (; e0 + 4 * 32 <= k; e0 += 4 * 32)
+      for (; e0 + PF_GNC * 32 <= k; e0 += PF_GNC * 32)
         chunk(e0, k, lpR + e0, ltR + e0, poR, binR, BoolTag<true>(), fast_tag,
-              IntTag<4>(), BoolTag<true>());
+              IntTag<PF_GNC>(), BoolTag<true>());
       // ragged tail (< 128 requests): predicated 1-request-per-lane chunks (one code copy:
       // fewer hot instructions for the instruction cache than 2-/1-request variants)
       const int32_t* pl = lpR + e0;
