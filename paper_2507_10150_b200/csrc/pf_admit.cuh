@@ -109,6 +109,7 @@ struct AdmitParams {
   int n_groups;              // G (shared mode)
   unsigned long long* gcost; // admit_group_kernel: [3][2·G] per-group cycles, counts (rotating)
   uint32_t cost_epoch;       // launch counter selecting the rotating cost buffers
+  uint32_t early_cycles;     // admit_group_kernel: SM-cycles the first CTAs finish early (0 = off)
   int cbits;                 // LOOK_SORTED: log2 of the coarse-index bucket count
   int csh;                   // LOOK_SORTED: bucket width 2^csh, smallest with (Lmax+1) >> csh ≤ 2^cbits
   const int32_t* dist_of;    // LOOK_GROUP  [n]

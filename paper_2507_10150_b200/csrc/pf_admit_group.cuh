@@ -605,12 +605,20 @@ __device__ __forceinline__ void group_one(const AdmitParams& p, const int lane, 
 // first launch (no measurements) splits by instance count. The partition only decides
 // which CTA computes an instance; every output is the same bit for bit.
 // (buffers: launch t reads cost[(t+2) % 3], adds to cost[t % 3], zeroes cost[(t+1) % 3])
-__device__ __forceinline__ int cost_cut(const AdmitParams& p, const float* wg, const float* cum, int b) {
-  // instance index at cumulative weight b·total/grid (b = grid → n); cum[g] = weight of
-  // groups < g, cum[G] = total
+__device__ __forceinline__ int cost_cut(const AdmitParams& p, const float* wg, const float* cum, int b,
+                                        float delta, int E) {
+  // instance index at cumulative weight f(b)·total (b = grid → n); cum[g] = weight of
+  // groups < g, cum[G] = total. f(b) = b/grid, except that with delta > 0 the first E CTAs
+  // take a (1 − delta) share each and the others split the remainder.
   const int G = p.n_groups;
-  if (b >= (int)gridDim.x) return p.n;
-  const float t = cum[G] * (float)b / (float)gridDim.x;
+  const int grid = (int)gridDim.x;
+  if (b >= grid) return p.n;
+  float f = (float)b / (float)grid;
+  if (delta > 0.f)
+    f = (b <= E) ? (float)b * (1.f - delta) / (float)grid
+                 : ((float)E * (1.f - delta) + (float)(b - E) * (1.f + delta * (float)E / (float)(grid - E))) /
+                       (float)grid;
+  const float t = cum[G] * f;
   int g = 0, len = G;  // last g with cum[g] ≤ t
   while (len > 1) {
     const int half = len >> 1;
@@ -686,8 +694,19 @@ __global__ void __launch_bounds__(NT, 1) admit_group_kernel(AdmitParams p) {
         }
         if (lane == 0) cum[0] = 0.f;
         __syncwarp();
-        lo = cost_cut(p, wg, cum, blockIdx.x);
-        hi = cost_cut(p, wg, cum, blockIdx.x + 1);
+        // early finishers (multi-rank contexts): the first E CTAs get delta less work so that
+        // their SMs are free for the side stream's history update, all-reduce and table
+        // build (launched by the caller to overlap this admit) before the admit ends; the
+        // kernel holds every SM's registers otherwise. delta = early_cycles / (expected SM
+        // busy cycles: total warp-cycles / (grid · warps per CTA)), at most 0.5.
+        float delta = 0.f;
+        const int E = ::min(16, (int)gridDim.x / 8);
+        if (p.early_cycles && E > 0) {
+          const float t_sm = cum[G] / ((float)gridDim.x * (float)(blockDim.x >> 5));
+          delta = t_sm > 0.f ? ::fminf(0.5f, (float)p.early_cycles / t_sm) : 0.f;
+        }
+        lo = cost_cut(p, wg, cum, blockIdx.x, delta, E);
+        hi = cost_cut(p, wg, cum, blockIdx.x + 1, delta, E);
       }
     }
     if (lane == 0) {

@@ -660,6 +660,12 @@ static pf_status launch_admit(pf_ctx* c, const int32_t* run_off, const int32_t* 
     const int grid = std::max(1, std::min(c->sms, C.n_instances));
     p.gcost = c->gcost;
     p.cost_epoch = c->cost_epoch++;
+    // multi-rank contexts: leave a few SMs free near the end for the overlapped side chain
+    // (PFSCHED_EARLY_CYCLES overrides; 0 = off)
+    {
+      const char* ec = getenv("PFSCHED_EARLY_CYCLES");
+      p.early_cycles = ec ? (uint32_t)atoi(ec) : (C.nranks > 1 ? 120000u : 0u);
+    }
     void* args[] = {&p};
     PF_CUDA(cudaLaunchKernel(group_fn(c, est), dim3(grid), dim3(c->gp_warps * 32), args, c->gp_smem, s));
     PF_CUDA(cudaGetLastError());
